@@ -1,0 +1,159 @@
+"""ctypes binding of libqtt.so (include/qtt.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (csrc/Makefile).  There is
+no CPU fallback: if the library or a CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import CapacityError, DeviceError, ShapeMismatchError, SolverError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt.so")
+
+_lib = None
+_lock = threading.Lock()
+
+QTT_OK, QTT_ERR_SHAPE, QTT_ERR_SOLVER, QTT_ERR_CAPACITY, QTT_ERR_CUDA, QTT_ERR_ARG = range(6)
+
+_P = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.c_int
+_VP = ctypes.c_void_p
+
+
+class QttStats(ctypes.Structure):
+    _fields_ = [
+        ("launches", ctypes.c_int64), ("k1_calls", ctypes.c_int64),
+        ("k1_flops", ctypes.c_double), ("k1_ms", ctypes.c_double),
+        ("env_calls", ctypes.c_int64), ("env_flops", ctypes.c_double), ("env_ms", ctypes.c_double),
+        ("cg_iters", ctypes.c_int64), ("cg_solves", ctypes.c_int64), ("chol_solves", ctypes.c_int64),
+        ("svd_calls", ctypes.c_int64), ("qr_calls", ctypes.c_int64), ("sweeps", ctypes.c_int64),
+        ("certifications", ctypes.c_int64),
+    ]
+
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+SIGNATURES = {
+    "qtt_version": [],
+    "qtt_last_error": [],
+    "qtt_ctx_create": [_I, ctypes.POINTER(_VP)],
+    "qtt_ctx_destroy": [_VP],
+    "qtt_ctx_synchronize": [_VP],
+    "qtt_ctx_stream": [_VP],
+    "qtt_ctx_set_profiling": [_VP, _I],
+    "qtt_ctx_get_stats": [_VP, ctypes.POINTER(QttStats)],
+    "qtt_ctx_reset_stats": [_VP],
+    "qtt_local_matvec": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
+    "qtt_env_left": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
+    "qtt_env_right": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
+    "qtt_psi_left": [_VP, _P, _P, _P] + [_I] * 5 + [_P],
+    "qtt_psi_right": [_VP, _P, _P, _P] + [_I] * 5 + [_P],
+    "qtt_local_rhs": [_VP, _P, _P, _P] + [_I] * 5 + [_P],
+    "qtt_local_dense": [_VP, _P, _P, _P] + [_I] * 8 + [_P],
+    "qtt_local_diag": [_VP, _P, _P, _P] + [_I] * 5 + [_P],
+    "qtt_mixed_residual": [_VP] + [_P] * 7 + [_I] * 10 + [_P],
+}
+_RESTYPES = {"qtt_last_error": ctypes.c_char_p, "qtt_ctx_stream": _VP}
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the shared library (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError(
+                f"{path} is missing; build it with __graft_entry__.build() "
+                "(the QTT engine has no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+        return lib
+
+
+def check(code: int):
+    if code == QTT_OK:
+        return
+    msg = _lib.qtt_last_error().decode(errors="replace")
+    if code == QTT_ERR_SHAPE:
+        raise ShapeMismatchError(msg)
+    if code == QTT_ERR_SOLVER:
+        raise SolverError(msg)
+    if code == QTT_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if code == QTT_ERR_ARG:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def call(name: str, *args):
+    lib = load_library()
+    check(getattr(lib, name)(*args))
+
+
+class Context:
+    """One engine context (CUDA stream + memory pool) on one device."""
+
+    def __init__(self, device: int = 0):
+        lib = load_library()
+        h = _VP()
+        check(lib.qtt_ctx_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            _lib.qtt_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        call("qtt_ctx_synchronize", self.handle)
+
+    @property
+    def stream(self) -> int:
+        return _lib.qtt_ctx_stream(self.handle)
+
+    def set_profiling(self, on: bool):
+        call("qtt_ctx_set_profiling", self.handle, 1 if on else 0)
+
+    def stats(self) -> dict:
+        s = QttStats()
+        call("qtt_ctx_get_stats", self.handle, ctypes.byref(s))
+        return {name: getattr(s, name) for name, _ in QttStats._fields_}
+
+    def reset_stats(self):
+        call("qtt_ctx_reset_stats", self.handle)
+
+
+_default_ctx = {}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _default_ctx.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _default_ctx[device] = ctx
+    return ctx
+
+
+def dptr(a: np.ndarray):
+    """ctypes double* of a C-contiguous float64 array."""
+    return a.ctypes.data_as(_P)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)

@@ -1,0 +1,145 @@
+"""Host wrappers of the device interface contractions (K1-K4 of SURVEY.md 2.3).
+
+Same names, argument order and layouts as the reference's private helpers in
+``ttfem/amen.py:108-160`` (which ``ttfem.amen`` re-exports under underscore names):
+    _phi_left_step(phi, xb, ac, xk)      amen.py:108
+    _phi_right_step(phi, xb, ac, xk)     amen.py:114
+    _psi_left_step(psi, xb, fc)          amen.py:120
+    _psi_right_step(psi, xb, fc)         amen.py:125
+    _local_rhs(psil, fc, psir)           amen.py:130
+    _local_matvec(phil, ac, phir, v)     amen.py:134
+    _local_dense(phil, ac, phir)         amen.py:140
+    _local_diag(phil, ac, phir)          amen.py:147
+    _mixed_residual(...)                 amen.py:154
+Each call copies its numpy inputs to the device, runs the sm_100a kernels and
+returns a fresh numpy array (inputs are never mutated).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ShapeMismatchError
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else nat.default_context()
+
+
+def _need(cond, msg):
+    if not cond:
+        raise ShapeMismatchError(msg)
+
+
+def local_matvec(phil, ac, phir, v, ctx=None):
+    phil, ac, phir, v = (nat.f64(a) for a in (phil, ac, phir, v))
+    rX, Ra, rU = phil.shape
+    _need(ac.ndim == 4 and ac.shape[0] == Ra, f"operator core {ac.shape} vs phil {phil.shape}")
+    _, m, n, Rb = ac.shape
+    rY, Rb2, rV = phir.shape
+    _need(Rb2 == Rb and v.shape == (rU, n, rV), f"local matvec shapes {phil.shape} {ac.shape} {phir.shape} {v.shape}")
+    y = np.empty((rX, m, rY))
+    nat.call("qtt_local_matvec", _ctx(ctx).handle, nat.dptr(phil), nat.dptr(ac), nat.dptr(phir),
+             nat.dptr(v), rX, Ra, rU, m, n, Rb, rY, rV, nat.dptr(y))
+    return y
+
+
+def phi_left_step(phi, xb, ac, xk, ctx=None):
+    phi, xb, ac, xk = (nat.f64(a) for a in (phi, xb, ac, xk))
+    rX, RA, rY = phi.shape
+    _, m, n, RB = ac.shape
+    rU = xb.shape[2]
+    rZ = xk.shape[2]
+    _need(xb.shape[:2] == (rX, m) and xk.shape[:2] == (rY, n) and ac.shape[0] == RA,
+          f"env left shapes {phi.shape} {xb.shape} {ac.shape} {xk.shape}")
+    out = np.empty((rU, RB, rZ))
+    nat.call("qtt_env_left", _ctx(ctx).handle, nat.dptr(phi), nat.dptr(xb), nat.dptr(ac), nat.dptr(xk),
+             rX, RA, rY, m, n, RB, rU, rZ, nat.dptr(out))
+    return out
+
+
+def phi_right_step(phi, xb, ac, xk, ctx=None):
+    phi, xb, ac, xk = (nat.f64(a) for a in (phi, xb, ac, xk))
+    rX, RA, rZ = phi.shape
+    Ra, m, n, RA2 = ac.shape
+    rB = xb.shape[0]
+    rY = xk.shape[0]
+    _need(RA2 == RA and xb.shape[1:] == (m, rX) and xk.shape[1:] == (n, rZ),
+          f"env right shapes {phi.shape} {xb.shape} {ac.shape} {xk.shape}")
+    out = np.empty((rB, Ra, rY))
+    nat.call("qtt_env_right", _ctx(ctx).handle, nat.dptr(phi), nat.dptr(xb), nat.dptr(ac), nat.dptr(xk),
+             rX, RA, rZ, m, n, Ra, rB, rY, nat.dptr(out))
+    return out
+
+
+def psi_left_step(psi, xb, fc, ctx=None):
+    psi, xb, fc = (nat.f64(a) for a in (psi, xb, fc))
+    rX, rF = psi.shape
+    _, m, rG = fc.shape
+    rU = xb.shape[2]
+    _need(fc.shape[0] == rF and xb.shape[:2] == (rX, m), f"psi left shapes {psi.shape} {xb.shape} {fc.shape}")
+    out = np.empty((rU, rG))
+    nat.call("qtt_psi_left", _ctx(ctx).handle, nat.dptr(psi), nat.dptr(xb), nat.dptr(fc),
+             rX, rF, m, rU, rG, nat.dptr(out))
+    return out
+
+
+def psi_right_step(psi, xb, fc, ctx=None):
+    psi, xb, fc = (nat.f64(a) for a in (psi, xb, fc))
+    rX, rG = psi.shape
+    rF, m, _ = fc.shape
+    rU = xb.shape[0]
+    _need(fc.shape[2] == rG and xb.shape[1:] == (m, rX), f"psi right shapes {psi.shape} {xb.shape} {fc.shape}")
+    out = np.empty((rU, rF))
+    nat.call("qtt_psi_right", _ctx(ctx).handle, nat.dptr(psi), nat.dptr(xb), nat.dptr(fc),
+             rX, rG, rU, m, rF, nat.dptr(out))
+    return out
+
+
+def local_rhs(psil, fc, psir, ctx=None):
+    psil, fc, psir = (nat.f64(a) for a in (psil, fc, psir))
+    rX, rF = psil.shape
+    _, m, rG = fc.shape
+    rY = psir.shape[0]
+    _need(fc.shape[0] == rF and psir.shape[1] == rG, f"local rhs shapes {psil.shape} {fc.shape} {psir.shape}")
+    out = np.empty((rX, m, rY))
+    nat.call("qtt_local_rhs", _ctx(ctx).handle, nat.dptr(psil), nat.dptr(fc), nat.dptr(psir),
+             rX, rF, m, rG, rY, nat.dptr(out))
+    return out
+
+
+def local_dense(phil, ac, phir, ctx=None):
+    phil, ac, phir = (nat.f64(a) for a in (phil, ac, phir))
+    rX, Ra, rU = phil.shape
+    _, m, n, Rb = ac.shape
+    rY, _, rV = phir.shape
+    out = np.empty((rX * m * rY, rU * n * rV))
+    nat.call("qtt_local_dense", _ctx(ctx).handle, nat.dptr(phil), nat.dptr(ac), nat.dptr(phir),
+             rX, Ra, rU, m, n, Rb, rY, rV, nat.dptr(out))
+    return out
+
+
+def local_diag(phil, ac, phir, ctx=None):
+    phil, ac, phir = (nat.f64(a) for a in (phil, ac, phir))
+    rX, Ra, _ = phil.shape
+    _, m, _, Rb = ac.shape
+    rY = phir.shape[0]
+    out = np.empty((rX, m, rY))
+    nat.call("qtt_local_diag", _ctx(ctx).handle, nat.dptr(phil), nat.dptr(ac), nat.dptr(phir),
+             rX, Ra, m, Rb, rY, nat.dptr(out))
+    return out
+
+
+def mixed_residual(psil, fc, psir, phil, ac, u, phir, ctx=None):
+    psil, fc, psir, phil, ac, u, phir = (nat.f64(a) for a in (psil, fc, psir, phil, ac, u, phir))
+    rX, rF = psil.shape
+    _, m, rG = fc.shape
+    rY = psir.shape[0]
+    _, Ra, rU = phil.shape
+    _, _, n, Rb = ac.shape
+    rV = phir.shape[2]
+    out = np.empty((rX, m, rY))
+    nat.call("qtt_mixed_residual", _ctx(ctx).handle, nat.dptr(psil), nat.dptr(fc), nat.dptr(psir),
+             nat.dptr(phil), nat.dptr(ac), nat.dptr(u), nat.dptr(phir),
+             rX, rF, rG, rY, Ra, rU, m, n, Rb, rV, nat.dptr(out))
+    return out
