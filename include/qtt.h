@@ -94,6 +94,72 @@ int qtt_mixed_residual(qtt_ctx* ctx, const double* psil, const double* f, const 
                        int rX, int rF, int rG, int rY, int Ra, int rU, int m, int n, int Rb, int rV,
                        double* out);
 
+/* ---- device-resident trains ------------------------------------------------ */
+/* Upload a train: core_ndim 3 (vector cores r0,n,r1) or 4 (operator cores R0,m,n,R1);
+ * shape holds order*core_ndim entries; data the row-major cores back to back.
+ * Replaces the TensorTrain / TTLinearOperator constructors (tt.py:110-189). */
+int qtt_train_upload(qtt_ctx* ctx, int order, int core_ndim, const int64_t* shape,
+                     const double* data, qtt_train** out);
+int qtt_train_info(const qtt_train* t, int* order, int* core_ndim, int64_t* numel);
+int qtt_train_shape(const qtt_train* t, int64_t* shape);
+int qtt_train_download(qtt_ctx* ctx, const qtt_train* t, double* data);
+int qtt_train_free(qtt_train* t);
+
+/* ---- TT algebra (tt.py) ----------------------------------------------------- */
+int qtt_orthogonalize_rl(qtt_ctx* ctx, const qtt_train* a, qtt_train** out); /* tt.py:396 */
+int qtt_tt_norm(qtt_ctx* ctx, const qtt_train* a, double* out);               /* tt.py:362 */
+int qtt_tt_dot(qtt_ctx* ctx, const qtt_train* a, const qtt_train* b, double* out); /* tt.py:351 */
+/* max_rank <= 0 means uncapped; operators are rounded over fused (m,n) modes */
+int qtt_tt_round(qtt_ctx* ctx, const qtt_train* a, double rel_tol, int max_rank,
+                 qtt_train** out);                                            /* tt.py:409, 506 */
+int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x,
+                 qtt_train** out);                                            /* tt.py:434 (policy=None) */
+/* ||Ax - f|| / ||f||; exact != 0 forces the QR-sweep norm of the explicit difference
+ * train; otherwise the Kronecker Gram path is used when it is provably accurate. */
+int qtt_residual_norm(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, const qtt_train* f,
+                      int exact, double* out, int* used_gram);               /* amen.py:87 */
+
+/* ---- dense factorizations of the sweep, host buffers --------------------------- */
+/* thin QR, numpy.linalg.qr conventions: q (rows x k), r (k x cols), k = min(rows, cols) */
+int qtt_qr(qtt_ctx* ctx, const double* mat, int rows, int cols, double* q, double* r);
+/* thin SVD: u (rows x k), s (k, descending), vt (k x cols)   (np.linalg.svd, tt.py:376) */
+int qtt_svd(qtt_ctx* ctx, const double* mat, int rows, int cols, double* u, double* s, double* vt);
+int qtt_rank_for_tolerance(const double* s, int n, double delta, int* out);  /* tt.py:386 */
+/* one local solve (amen.py:170): phil (rl,R0,rl), A (R0,m,m,R1), phir (rr,R1,rr),
+ * rhs/prev (rl,m,rr).  Direct (dense + Cholesky) or Jacobi-PCG per the reference rule. */
+int qtt_local_solve(qtt_ctx* ctx, const double* phil, const double* A, const double* phir,
+                    const double* rhs, const double* prev, int rl, int R0, int m, int R1, int rr,
+                    int iterative, int direct_dim_cap, double residual_tol, int iter_cap,
+                    double* u, double* lam, int* iterations);
+
+/* ---- the solve (amen.py:394-510) --------------------------------------------- */
+typedef struct {
+  double residual_tol;    /* AmenConfig.residual_tol     (amen.py:53) */
+  int max_sweeps;         /* AmenConfig.max_sweeps       (amen.py:54) */
+  int enrichment_rank;    /* AmenConfig.enrichment_rank  (amen.py:55) */
+  int local_iterative;    /* local_solver == "iterative" (amen.py:56) */
+  int direct_dim_cap;     /* (amen.py:57) */
+  int local_iter_cap;     /* (amen.py:58) */
+  double round_tol;       /* rounding.rel_tolerance      (amen.py:59) */
+  int round_max_rank;     /* rounding.max_rank, <= 0: None */
+  int stagnation_strikes; /* (amen.py:64) */
+} qtt_amen_params;
+
+typedef struct {
+  int converged;
+  int sweeps_used;
+  double final_relative_residual;
+  int certifications_gram, certifications_exact;
+  int64_t draws_used;
+} qtt_amen_report;
+
+/* draws: the numpy default_rng(seed).standard_normal stream in the reference's
+ * consumption order (probe vectors, then z cores, then z redraws); rank_hist has
+ * room for max_sweeps*(order+1) ints and res_hist for max_sweeps doubles. */
+int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const qtt_train* x0,
+                   const qtt_amen_params* prm, const double* draws, int64_t n_draws,
+                   qtt_train** x_out, qtt_amen_report* rep, int32_t* rank_hist, double* res_hist);
+
 #ifdef __cplusplus
 }
 #endif

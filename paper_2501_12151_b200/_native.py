@@ -56,7 +56,44 @@ SIGNATURES = {
     "qtt_local_dense": [_VP, _P, _P, _P] + [_I] * 8 + [_P],
     "qtt_local_diag": [_VP, _P, _P, _P] + [_I] * 5 + [_P],
     "qtt_mixed_residual": [_VP] + [_P] * 7 + [_I] * 10 + [_P],
+    "qtt_train_upload": [_VP, _I, _I, ctypes.POINTER(ctypes.c_int64), _P, ctypes.POINTER(_VP)],
+    "qtt_train_info": [_VP, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(ctypes.c_int64)],
+    "qtt_train_shape": [_VP, ctypes.POINTER(ctypes.c_int64)],
+    "qtt_train_download": [_VP, _VP, _P],
+    "qtt_train_free": [_VP],
+    "qtt_orthogonalize_rl": [_VP, _VP, ctypes.POINTER(_VP)],
+    "qtt_tt_norm": [_VP, _VP, _P],
+    "qtt_tt_dot": [_VP, _VP, _VP, _P],
+    "qtt_tt_round": [_VP, _VP, ctypes.c_double, _I, ctypes.POINTER(_VP)],
+    "qtt_tt_apply": [_VP, _VP, _VP, ctypes.POINTER(_VP)],
+    "qtt_residual_norm": [_VP, _VP, _VP, _VP, _I, _P, ctypes.POINTER(_I)],
+    "qtt_qr": [_VP, _P, _I, _I, _P, _P],
+    "qtt_svd": [_VP, _P, _I, _I, _P, _P, _P],
+    "qtt_rank_for_tolerance": [_P, _I, ctypes.c_double, ctypes.POINTER(_I)],
+    "qtt_local_solve": [_VP, _P, _P, _P, _P, _P] + [_I] * 7 + [ctypes.c_double, _I, _P, _P,
+                                                                 ctypes.POINTER(_I)],
+    "qtt_amen_solve": [_VP, _VP, _VP, _VP, ctypes.c_void_p, _P, ctypes.c_int64, ctypes.POINTER(_VP),
+                       ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), _P],
 }
+
+
+class AmenParams(ctypes.Structure):
+    _fields_ = [
+        ("residual_tol", ctypes.c_double), ("max_sweeps", ctypes.c_int),
+        ("enrichment_rank", ctypes.c_int), ("local_iterative", ctypes.c_int),
+        ("direct_dim_cap", ctypes.c_int), ("local_iter_cap", ctypes.c_int),
+        ("round_tol", ctypes.c_double), ("round_max_rank", ctypes.c_int),
+        ("stagnation_strikes", ctypes.c_int),
+    ]
+
+
+class AmenReport(ctypes.Structure):
+    _fields_ = [
+        ("converged", ctypes.c_int), ("sweeps_used", ctypes.c_int),
+        ("final_relative_residual", ctypes.c_double),
+        ("certifications_gram", ctypes.c_int), ("certifications_exact", ctypes.c_int),
+        ("draws_used", ctypes.c_int64),
+    ]
 _RESTYPES = {"qtt_last_error": ctypes.c_char_p, "qtt_ctx_stream": _VP}
 
 

@@ -1,0 +1,884 @@
+// Device AMEn sweep and driver (amen.py:163-510), orchestrated from C++ on the
+// context stream.  Host round trips happen only where the reference makes a
+// data-dependent decision: SVD rank choice, Cholesky pivot check, CG stopping
+// (polled in chunks), the per-sweep estimate and the certification.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "amen.cuh"
+#include "contract.cuh"
+#include "gemm.cuh"
+#include "linalg.cuh"
+
+namespace qtt {
+
+const double* DrawStream::take(long long k) {
+  if (pos + k > n) throw Error(QTT_ERR_ARG, "random draw stream exhausted");
+  const double* out = p + pos;
+  pos += k;
+  return out;
+}
+
+namespace {
+
+
+// ------------------------------------------------------------------ CG kernels
+// Device state in Ctx::scal: [0] rho [1] alpha [2] rnorm [3] beta
+// Ctx::flags: [0] done [1] iterations
+constexpr int RB = 148;  // reduction blocks
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// two simultaneous block sums (256 threads)
+__device__ void block_sum2(double& a, double& b, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = wsum(a);
+  b = wsum(b);
+  __syncthreads();
+  if (lane == 0) { red[warp] = a; red[8 + warp] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < 8 ? red[lane] : 0.0, y = lane < 8 ? red[8 + lane] : 0.0;
+    x = wsum(x);
+    y = wsum(y);
+    if (lane == 0) { red[16] = x; red[17] = y; }
+  }
+  __syncthreads();
+  a = red[16];
+  b = red[17];
+}
+
+// r0: residual;  computes z = invd*r, p = z, rho = r.z, rnorm = |r|; done if rnorm < atol.
+__global__ void __launch_bounds__(256) cg_start_kernel(const double* r, const double* invd, double* z,
+                                                       double* p, long long n, double atol, double* part,
+                                                       unsigned* counter, double* scal, int* flags) {
+  __shared__ double red[20];
+  __shared__ bool last;
+  double rr = 0, rz = 0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const double ri = r[i], zi = ri * invd[i];
+    z[i] = zi;
+    p[i] = zi;
+    rr += ri * ri;
+    rz += ri * zi;
+  }
+  block_sum2(rr, rz, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = rz;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) {
+    a += ((volatile double*)part)[2 * i];
+    b += ((volatile double*)part)[2 * i + 1];
+  }
+  block_sum2(a, b, red);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    const double rn = sqrt(a);
+    scal[2] = rn;
+    scal[0] = b;
+    flags[1] = 0;
+    flags[0] = (rn < atol) ? 1 : 0;
+  }
+}
+
+// alpha = rho / (p.q)
+__global__ void __launch_bounds__(256) cg_alpha_kernel(const double* p, const double* q, long long n,
+                                                       double* part, unsigned* counter, double* scal,
+                                                       const int* flags) {
+  if (flags[0]) return;
+  __shared__ double red[20];
+  __shared__ bool last;
+  double pq = 0, dummy = 0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    pq += p[i] * q[i];
+  block_sum2(pq, dummy, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = pq;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) a += ((volatile double*)part)[i];
+  block_sum2(a, b, red);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    scal[1] = scal[0] / a;
+  }
+}
+
+// x += alpha p; r -= alpha q; z = invd r; then rnorm, rho_new; stopping; beta.
+__global__ void __launch_bounds__(256) cg_update_kernel(double* x, double* r, double* z, const double* p,
+                                                        const double* q, const double* invd, long long n,
+                                                        double atol, int maxiter, double* part,
+                                                        unsigned* counter, double* scal, int* flags) {
+  if (flags[0]) return;
+  __shared__ double red[20];
+  __shared__ bool last;
+  const double alpha = scal[1];
+  double rr = 0, rz = 0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    const double zi = ri * invd[i];
+    z[i] = zi;
+    rr += ri * ri;
+    rz += ri * zi;
+  }
+  block_sum2(rr, rz, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = rr;
+    part[2 * blockIdx.x + 1] = rz;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) {
+    a += ((volatile double*)part)[2 * i];
+    b += ((volatile double*)part)[2 * i + 1];
+  }
+  block_sum2(a, b, red);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    const int it = flags[1] + 1;
+    flags[1] = it;
+    const double rn = sqrt(a);
+    scal[2] = rn;
+    if (rn < atol || it >= maxiter) {
+      flags[0] = 1;
+    } else {
+      scal[3] = b / scal[0];
+      scal[0] = b;
+    }
+  }
+}
+
+__global__ void cg_dir_kernel(double* p, const double* z, long long n, const double* scal,
+                              const int* flags) {
+  if (flags[0]) return;
+  const double beta = scal[3];
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    p[i] = z[i] + beta * p[i];
+}
+
+// invd = 1 / (d > 0 ? d : 1)   (amen.py:197-199)
+__global__ void jacobi_inv_kernel(const double* d, double* invd, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    invd[i] = 1.0 / (d[i] > 0 ? d[i] : 1.0);
+}
+
+__global__ void sum_abs_kernel(const double* a, long long n, double* out) {
+  // non-negative doubles order like their bit patterns: integer atomicMax gives max|a|
+  double m = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    m = fmax(m, fabs(a[i]));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 16));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  if ((threadIdx.x & 31) == 0 && m > 0)
+    atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(m));
+}
+
+// Build aug = [U[:, :r] | E] where E is given as a strided view (rows x re).
+__global__ void build_aug_kernel(const double* U, int ldu, int r, CMatView E, double* aug, int rows) {
+  const int cols = r + E.cols;
+  const long long total = (long long)rows * cols;
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += (long long)gridDim.x * 256) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    aug[e] = j < r ? U[(long long)i * ldu + j] : E.p[i * E.rs + (j - r) * E.cs];
+  }
+}
+
+inline int grid_for(long long n) {
+  return (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 1184));
+}
+
+// ------------------------------------------------------------------ helpers
+struct Env {
+  int b = 1, o = 1, k = 1;  // phi: (bra, op, ket); psi: (bra, rhs, 1)
+  DBuf d;
+};
+
+Env unit_env(Ctx& c) {
+  Env e;
+  e.d.alloc(1, c.stream);
+  fill(c, e.d.p, 1, 1.0);
+  return e;
+}
+
+struct EventTimer {
+  Ctx& c;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
+  size_t used = 0;
+  explicit EventTimer(Ctx& cc) : c(cc) {}
+  ~EventTimer() {
+    for (auto& p : pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  }
+  int start() {
+    if (used == pairs.size()) {
+      cudaEvent_t a, b;
+      QTT_CUDA(cudaEventCreate(&a));
+      QTT_CUDA(cudaEventCreate(&b));
+      pairs.push_back({a, b});
+    }
+    QTT_CUDA(cudaEventRecord(pairs[used].first, c.stream));
+    return (int)used++;
+  }
+  void stop(int i) { QTT_CUDA(cudaEventRecord(pairs[i].second, c.stream)); }
+  double ms(int i) {
+    float t = 0;
+    QTT_CUDA(cudaEventElapsedTime(&t, pairs[i].first, pairs[i].second));
+    return t;
+  }
+  void reset() { used = 0; }
+};
+
+}  // namespace
+
+DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, const double* prev_p,
+                        const AmenParams& prm_, int sweep_, int k, double& lam, int& iters,
+                        bool profile) {
+  EventTimer timer_(c_);
+  const int m = L.m;
+  const long long dim = (long long)L.lb * m * L.rb;
+  DBuf mv_scratch;
+  auto matvec = [&](const double* v, double* y, double alpha, double beta, const int* skip) {
+    const long long need = local_matvec_scratch(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk) +
+                           (long long)L.lb * L.m * L.rb * 8;
+    if (mv_scratch.n < need) mv_scratch.alloc(need, c_.stream);
+    DBuf& sc = mv_scratch;
+    local_matvec(L.phil, L.lb, L.lo, L.lk, L.Ap, L.m, L.n, L.R1, L.phir, L.rb, L.rk, v, y, alpha, beta,
+                 {sc.p, sc.n}, c_.stream, skip);
+  };
+  iters = 0;
+  DBuf u(dim, c_.stream);
+  if (!prm_.local_iterative && dim <= prm_.direct_dim_cap) {
+    // ---- direct: dense local matrix + Cholesky (amen.py:181-191)
+    DBuf M(dim * dim, c_.stream);
+    DBuf sc(local_dense_scratch(L.lb, L.lo, L.lk, L.m, L.n, L.R1), c_.stream);
+    local_dense(L.phil, L.lb, L.lo, L.lk, L.A, L.m, L.n, L.R1, L.phir, L.rb, L.rk, M.p, {sc.p, sc.n},
+                c_.stream);
+    max_abs_row_sum(c_, M.p, (int)dim, dim, c_.scal + 8);
+    potrf_lower(c_, M.p, (int)dim, dim, c_.flags + 3);
+    QTT_CUDA(cudaMemcpyAsync(u.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
+    potrs_lower(c_, M.p, (int)dim, dim, u.p);
+    double* pin = c_.host_scalars(2);
+    QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 8, 8, cudaMemcpyDeviceToHost, c_.stream));
+    QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 3, 4, cudaMemcpyDeviceToHost, c_.stream));
+    c_.sync();
+    lam = pin[0];
+    int info;
+    std::memcpy(&info, pin + 1, 4);
+    if (info != 0)
+      throw Error(QTT_ERR_SOLVER, "local system not positive definite at sweep " + std::to_string(sweep_) +
+                                      ", core " + std::to_string(k) + " (dim " + std::to_string(dim) +
+                                      "): leading minor of order " + std::to_string(info) +
+                                      " is not positive");
+    return u;
+  }
+  // ---- iterative: Jacobi-PCG (amen.py:192-214, SciPy cg recurrence)
+  c_.stats.cg_solves++;
+  DBuf diag(dim, c_.stream), invd(dim, c_.stream);
+  {
+    DBuf sc((long long)L.lb * m * L.R1, c_.stream);
+    local_diag(L.phil, L.lb, L.lo, L.A, m, L.R1, L.phir, L.rb, diag.p, {sc.p, sc.n}, c_.stream);
+  }
+  sum(c_, diag.p, dim, c_.scal + 8);  // lam = trace (before the non-positive replacement)
+  jacobi_inv_kernel<<<grid_for(dim), 256, 0, c_.stream>>>(diag.p, invd.p, dim);
+  QTT_CHECK_LAUNCH();
+  nrm2(c_, rhs_p, dim, c_.scal + 9);
+  QTT_CUDA(cudaMemsetAsync(c_.scal + 10, 0, 8, c_.stream));
+  sum_abs_kernel<<<grid_for(dim), 256, 0, c_.stream>>>(prev_p, dim, c_.scal + 10);
+  QTT_CHECK_LAUNCH();
+  double h[3];
+  read_scalars(c_, c_.scal + 8, 3, h);
+  lam = h[0];
+  const double bnorm = h[1];
+  const bool xany = h[2] > 0;
+  if (bnorm == 0.0) {  // scipy returns b itself
+    QTT_CUDA(cudaMemcpyAsync(u.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
+    return u;
+  }
+  const double rtol = std::max(0.05 * prm_.residual_tol, 1e-13);
+  const double atol = rtol * bnorm;
+  DBuf r(dim, c_.stream), z(dim, c_.stream), p(dim, c_.stream), q(dim, c_.stream);
+  QTT_CUDA(cudaMemcpyAsync(u.p, prev_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
+  QTT_CUDA(cudaMemcpyAsync(r.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
+  const double kflops = local_matvec_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk);
+  int* flags = c_.flags;
+  if (xany) {  // r = b - A x0
+    int t = profile ? timer_.start() : -1;
+    matvec(u.p, r.p, -1.0, 1.0, nullptr);
+    if (t >= 0) timer_.stop(t);
+    c_.stats.k1_calls++;
+    c_.stats.k1_flops += kflops;
+  }
+  const int rb = (int)std::min<long long>(RB, cdiv(dim, 256));
+  cg_start_kernel<<<rb, 256, 0, c_.stream>>>(r.p, invd.p, z.p, p.p, dim, atol, c_.red_partial,
+                                             c_.red_counter, c_.scal, flags);
+  QTT_CHECK_LAUNCH();
+  const int maxiter = prm_.local_iter_cap;
+  constexpr int CHUNK = 8;
+  std::vector<int> tidx;
+  int done_iters = 0;
+  if (maxiter <= 0) {
+    done_iters = 0;
+  } else {
+    for (int launched = 0; launched < maxiter;) {
+      const int nlaunch = std::min(CHUNK, maxiter - launched);
+      for (int i = 0; i < nlaunch; ++i) {
+        int t = profile ? timer_.start() : -1;
+        matvec(p.p, q.p, 1.0, 0.0, flags);
+        if (t >= 0) { timer_.stop(t); tidx.push_back(t); }
+        cg_alpha_kernel<<<rb, 256, 0, c_.stream>>>(p.p, q.p, dim, c_.red_partial, c_.red_counter, c_.scal,
+                                                   flags);
+        QTT_CHECK_LAUNCH();
+        cg_update_kernel<<<rb, 256, 0, c_.stream>>>(u.p, r.p, z.p, p.p, q.p, invd.p, dim, atol, maxiter,
+                                                    c_.red_partial, c_.red_counter, c_.scal, flags);
+        QTT_CHECK_LAUNCH();
+        cg_dir_kernel<<<grid_for(dim), 256, 0, c_.stream>>>(p.p, z.p, dim, c_.scal, flags);
+        QTT_CHECK_LAUNCH();
+      }
+      launched += nlaunch;
+      int* pin = (int*)c_.host_scalars(1);
+      QTT_CUDA(cudaMemcpyAsync(pin, flags, 8, cudaMemcpyDeviceToHost, c_.stream));
+      c_.sync();
+      done_iters = pin[1];
+      if (pin[0]) break;
+    }
+  }
+  c_.stats.cg_iters += done_iters;
+  c_.stats.k1_calls += done_iters;
+  c_.stats.k1_flops += kflops * done_iters;
+  iters = done_iters;
+  if (profile) {
+    c_.sync();
+    if (xany) c_.stats.k1_ms += timer_.ms(0);
+    for (int i = 0; i < done_iters && i < (int)tidx.size(); ++i) c_.stats.k1_ms += timer_.ms(tidx[i]);
+  }
+  return u;
+}
+
+namespace {
+
+class Solver {
+ public:
+  Solver(Ctx& c, Train& A, const Train& f, const AmenParams& prm, DrawStream& draws)
+      : c_(c), A_(A), f_(f), prm_(prm), draws_(draws), timer_(c) {
+    K_ = A.order();
+    dims_ = f.dims();
+  }
+
+  Train run(const Train* x0, AmenResult& res);
+
+ private:
+  Ctx& c_;
+  Train& A_;
+  const Train& f_;
+  AmenParams prm_;
+  DrawStream& draws_;
+  EventTimer timer_;
+  int K_ = 0;
+  std::vector<int> dims_;
+  std::vector<Core> x_, z_;
+  std::vector<Env> phi_, phiz_, psi_, psiz_;
+  double lam_max_ = 0.0, nf_ = 0.0;
+  int sweep_ = 0;
+
+  void probe_symmetry();
+  Train default_x0();
+  std::vector<Core> init_z();
+  void full_prepass(bool forward, bool xenvs, bool zenvs);
+  double sweep(bool forward);
+  void env_step_left(int k, bool xenvs, bool zenvs);
+  void env_step_right(int k, bool xenvs, bool zenvs);
+  Env phi_left(const Env& phi, const Core& bra, int k, const Core& ket);
+  Env phi_right(const Env& phi, const Core& bra, int k, const Core& ket);
+  Env psi_left_(const Env& psi, const Core& bra, int k);
+  Env psi_right_(const Env& psi, const Core& bra, int k);
+  DBuf local_rhs_(const Env& pl, int k, const Env& pr);
+  DBuf mixed_res(const Env& psl, int k, const Env& psr, const Env& pl, const DBuf& u, int rl, int rr,
+                 const Env& pr);
+  void matvec(const Env& pl, int k, const Env& pr, const double* v, double* y, double alpha,
+              double beta, const int* skip, bool timed);
+  DBuf solve_local(int k, const DBuf& rhs, const Core& prev, double& lam);
+};
+
+Env Solver::phi_left(const Env& phi, const Core& bra, int k, const Core& ket) {
+  const Core& a = A_.cores[k];
+  Env out;
+  out.b = bra.r1; out.o = a.r1; out.k = ket.r1;
+  out.d.alloc((long long)out.b * out.o * out.k, c_.stream);
+  DBuf sc(env_left_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r1, ket.r1) +
+              (long long)out.b * out.o * out.k * 4, c_.stream);
+  int t = c_.profiling ? timer_.start() : -1;
+  env_left(phi.d.p, phi.b, phi.o, phi.k, bra.d.p, bra.r1, A_.Ap[k].p, a.m, a.n, a.r1, ket.d.p, ket.r1,
+           out.d.p, {sc.p, sc.n}, c_.stream);
+  if (t >= 0) {
+    timer_.stop(t);
+    c_.sync();
+    c_.stats.env_ms += timer_.ms(t);
+    timer_.reset();
+  }
+  c_.stats.env_calls++;
+  c_.stats.env_flops += env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r1, bra.r1, ket.r1);
+  return out;
+}
+
+Env Solver::phi_right(const Env& phi, const Core& bra, int k, const Core& ket) {
+  const Core& a = A_.cores[k];
+  Env out;
+  out.b = bra.r0; out.o = a.r0; out.k = ket.r0;
+  out.d.alloc((long long)out.b * out.o * out.k, c_.stream);
+  DBuf sc(env_right_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r0, ket.r0) +
+              (long long)out.b * out.o * out.k * 4, c_.stream);
+  int t = c_.profiling ? timer_.start() : -1;
+  env_right(phi.d.p, phi.b, phi.o, phi.k, bra.d.p, bra.r0, A_.Aq[k].p, a.m, a.n, a.r0, ket.d.p, ket.r0,
+            out.d.p, {sc.p, sc.n}, c_.stream);
+  if (t >= 0) {
+    timer_.stop(t);
+    c_.sync();
+    c_.stats.env_ms += timer_.ms(t);
+    timer_.reset();
+  }
+  c_.stats.env_calls++;
+  c_.stats.env_flops += env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r0, bra.r0, ket.r0);
+  return out;
+}
+
+Env Solver::psi_left_(const Env& psi, const Core& bra, int k) {
+  const Core& fk = f_.cores[k];
+  Env out;
+  out.b = bra.r1; out.o = fk.r1;
+  out.d.alloc((long long)out.b * out.o, c_.stream);
+  DBuf sc((long long)psi.b * fk.m * fk.r1 + (long long)out.b * out.o * 8, c_.stream);
+  psi_left(psi.d.p, psi.b, psi.o, bra.d.p, bra.m, bra.r1, fk.d.p, fk.r1, out.d.p, {sc.p, sc.n}, c_.stream);
+  return out;
+}
+
+Env Solver::psi_right_(const Env& psi, const Core& bra, int k) {
+  const Core& fk = f_.cores[k];
+  Env out;
+  out.b = bra.r0; out.o = fk.r0;
+  out.d.alloc((long long)out.b * out.o, c_.stream);
+  DBuf sc((long long)fk.r0 * fk.m * psi.b + (long long)out.b * out.o * 8, c_.stream);
+  psi_right(psi.d.p, psi.b, psi.o, bra.d.p, bra.r0, bra.m, fk.d.p, fk.r0, out.d.p, {sc.p, sc.n}, c_.stream);
+  return out;
+}
+
+DBuf Solver::local_rhs_(const Env& pl, int k, const Env& pr) {
+  const Core& fk = f_.cores[k];
+  DBuf out((long long)pl.b * fk.m * pr.b, c_.stream);
+  DBuf sc((long long)pl.b * fk.m * fk.r1 + (long long)pl.b * fk.m * pr.b * 8, c_.stream);
+  local_rhs(pl.d.p, pl.b, pl.o, fk.d.p, fk.m, fk.r1, pr.d.p, pr.b, out.p, {sc.p, sc.n}, c_.stream);
+  return out;
+}
+
+void Solver::matvec(const Env& pl, int k, const Env& pr, const double* v, double* y, double alpha,
+                    double beta, const int* skip, bool timed) {
+  const Core& a = A_.cores[k];
+  const long long need = local_matvec_scratch(pl.b, pl.o, pl.k, a.m, a.n, a.r1, pr.b, pr.k) +
+                         (long long)pl.b * a.m * pr.b * 8;
+  DBuf sc(need, c_.stream);
+  local_matvec(pl.d.p, pl.b, pl.o, pl.k, A_.Ap[k].p, a.m, a.n, a.r1, pr.d.p, pr.b, pr.k, v, y, alpha,
+               beta, {sc.p, sc.n}, c_.stream, skip);
+  (void)timed;
+}
+
+DBuf Solver::mixed_res(const Env& psl, int k, const Env& psr, const Env& pl, const DBuf& u, int rl,
+                       int rr, const Env& pr) {
+  (void)rl; (void)rr;
+  DBuf out = local_rhs_(psl, k, psr);
+  const Core& a = A_.cores[k];
+  int t = c_.profiling ? timer_.start() : -1;
+  matvec(pl, k, pr, u.p, out.p, -1.0, 1.0, nullptr, false);
+  if (t >= 0) {
+    timer_.stop(t);
+    c_.sync();
+    c_.stats.k1_ms += timer_.ms(t);
+    timer_.reset();
+  }
+  c_.stats.k1_calls++;
+  c_.stats.k1_flops += local_matvec_flops(pl.b, pl.o, pl.k, a.m, a.n, a.r1, pr.b, pr.k);
+  return out;
+}
+
+DBuf Solver::solve_local(int k, const DBuf& rhs, const Core& prev, double& lam) {
+  const Env& pl = phi_[k];
+  const Env& pr = phi_[k + 1];
+  const Core& a = A_.cores[k];
+  LocalSystem L{pl.d.p, pl.b, pl.o, pl.k, a.d.p, A_.Ap[k].p, a.r0, a.m, a.n, a.r1, pr.d.p, pr.b, pr.o, pr.k};
+  int iters = 0;
+  return solve_local_system(c_, L, rhs.p, prev.d.p, prm_, sweep_, k, lam, iters, c_.profiling);
+}
+
+// ------------------------------------------------------------------ env plumbing
+void Solver::env_step_left(int k, bool xenvs, bool zenvs) {
+  if (xenvs) {
+    phi_[k + 1] = phi_left(phi_[k], x_[k], k, x_[k]);
+    psi_[k + 1] = psi_left_(psi_[k], x_[k], k);
+  }
+  if (zenvs) {
+    phiz_[k + 1] = phi_left(phiz_[k], z_[k], k, x_[k]);
+    psiz_[k + 1] = psi_left_(psiz_[k], z_[k], k);
+  }
+}
+
+void Solver::env_step_right(int k, bool xenvs, bool zenvs) {
+  if (xenvs) {
+    phi_[k] = phi_right(phi_[k + 1], x_[k], k, x_[k]);
+    psi_[k] = psi_right_(psi_[k + 1], x_[k], k);
+  }
+  if (zenvs) {
+    phiz_[k] = phi_right(phiz_[k + 1], z_[k], k, x_[k]);
+    psiz_[k] = psi_right_(psiz_[k + 1], z_[k], k);
+  }
+}
+
+// amen.py:300-321.  The reference rebuilds every opposite-side environment at the
+// start of each sweep; those equal the ones the previous sweep already produced
+// (each depends only on cores that sweep no longer touches), so they are kept
+// resident and only rebuilt when their inputs changed (first sweep, z redraw).
+void Solver::full_prepass(bool forward, bool xenvs, bool zenvs) {
+  if (forward)
+    for (int k = K_ - 1; k >= 1; --k) env_step_right(k, xenvs, zenvs);
+  else
+    for (int k = 0; k < K_ - 1; ++k) env_step_left(k, xenvs, zenvs);
+}
+
+double Solver::sweep(bool forward) {
+  double est = 0.0;
+  const double rel = prm_.round_tol;
+  const int cap = prm_.round_max_rank;
+  for (int step = 0; step < K_; ++step) {
+    const int k = forward ? step : K_ - 1 - step;
+    const int rl = x_[k].r0, m = x_[k].m, rr = x_[k].r1;
+    DBuf rhs = local_rhs_(psi_[k], k, psi_[k + 1]);
+    double lam = 0.0;
+    DBuf u = solve_local(k, rhs, x_[k], lam);
+    lam_max_ = std::max(lam_max_, lam);
+    const bool have_dabs = K_ > 1 && lam_max_ > 0;
+    const double dabs = have_dabs ? prm_.residual_tol * nf_ / (lam_max_ * std::sqrt((double)(K_ - 1))) : 0.0;
+
+    // zeta: local residual in the z bases (rz_l, m, rz_r)
+    DBuf zeta = mixed_res(psiz_[k], k, psiz_[k + 1], phiz_[k], u, rl, rr, phiz_[k + 1]);
+    const int zl = phiz_[k].b, zr = phiz_[k + 1].b;
+    const bool last = forward ? (k == K_ - 1) : (k == 0);
+    if (last) {
+      Core nu;
+      nu.r0 = rl; nu.m = m; nu.n = 1; nu.r1 = rr;
+      nu.d = std::move(u);
+      x_[k] = std::move(nu);
+      Core nz;
+      nz.r0 = zl; nz.m = m; nz.n = 1; nz.r1 = zr;
+      nz.d = std::move(zeta);
+      nrm2(c_, nz.d.p, nz.numel(), c_.scal + 12);
+      z_[k] = std::move(nz);
+      read_scalars(c_, c_.scal + 12, 1, &est);
+      break;
+    }
+
+    // enrichment from the mixed x/z residual, and the truncated split of u
+    DBuf enr;
+    int rows, cols, ecols;
+    CMatView uview, eview;
+    if (forward) {
+      enr = mixed_res(psi_[k], k, psiz_[k + 1], phi_[k], u, rl, rr, phiz_[k + 1]);  // (rl, m, zr)
+      rows = rl * m; cols = rr; ecols = zr;
+      uview = crowmajor(u.p, rows, cols);
+      eview = crowmajor(enr.p, rows, ecols);
+    } else {
+      enr = mixed_res(psiz_[k], k, psi_[k + 1], phiz_[k], u, rl, rr, phi_[k + 1]);  // (zl, m, rr)
+      rows = m * rr; cols = rl; ecols = zl;
+      uview = ctrans(crowmajor(u.p, rl, m * rr));
+      eview = ctrans(crowmajor(enr.p, zl, m * rr));
+    }
+    const int kk = std::min(rows, cols);
+    DBuf U((long long)rows * kk, c_.stream), s(kk, c_.stream), Vt((long long)kk * cols, c_.stream);
+    svd(c_, uview, rowmajor(U.p, rows, kk), s.p, rowmajor(Vt.p, kk, cols));
+    std::vector<double> hs(kk);
+    read_scalars(c_, s.p, kk, hs.data());
+    double norm = 0.0;
+    for (double v : hs) norm += v * v;
+    norm = std::sqrt(norm);
+    int r;
+    DBuf w;
+    if (norm == 0.0) {  // amen.py:225-226
+      r = 1;
+      w.alloc(cols, c_.stream);
+      fill(c_, w.p, cols, 0.0);
+    } else {
+      double delta = rel * norm;
+      if (have_dabs) delta = std::min(delta, dabs);
+      r = rank_for_tolerance(hs.data(), kk, delta);
+      if (cap > 0) r = std::min(r, cap);
+      r = std::max(r, 1);
+      w.alloc((long long)r * cols, c_.stream);
+      scale_rows(c_, Vt.p, cols, s.p, r, cols, w.p, cols);
+    }
+    // q, R = qr([Q | enrich])
+    const int acols = r + ecols;
+    DBuf aug((long long)rows * acols, c_.stream);
+    build_aug_kernel<<<grid_for((long long)rows * acols), 256, 0, c_.stream>>>(U.p, kk, r, eview, aug.p, rows);
+    QTT_CHECK_LAUNCH();
+    const int kq = std::min(rows, acols);
+    DBuf Q((long long)rows * kq, c_.stream), R((long long)kq * acols, c_.stream);
+    qr(c_, crowmajor(aug.p, rows, acols), rowmajor(Q.p, rows, kq), rowmajor(R.p, kq, acols));
+    // absorb = R[:, :r] @ w   (kq x cols)
+    DBuf absorb((long long)kq * cols, c_.stream);
+    {
+      GemmArgs g;
+      g.M = kq; g.N = cols; g.K = r;
+      gemm_set_A(g, R.p, acols, false);
+      gemm_set_B(g, w.p, cols, false);
+      gemm_set_C(g, absorb.p, cols);
+      gemm(g, c_.stream);
+    }
+    // z core from qr(zeta)
+    if (forward) {
+      const int zrows = zl * m, kz = std::min(zrows, zr);
+      Core nz = make_core(c_, zl, m, 1, kz);
+      qr(c_, crowmajor(zeta.p, zrows, zr), rowmajor(nz.d.p, zrows, kz), MatView{});
+      z_[k] = std::move(nz);
+      // x_k = q (rl, m, kq);  x_{k+1} = absorb @ x_{k+1}
+      Core nx;
+      nx.r0 = rl; nx.m = m; nx.n = 1; nx.r1 = kq;
+      nx.d = std::move(Q);
+      x_[k] = std::move(nx);
+      Core& nxt = x_[k + 1];
+      Core nn = make_core(c_, kq, nxt.m, 1, nxt.r1);
+      GemmArgs g;
+      g.M = kq; g.N = nxt.m * nxt.r1; g.K = cols;
+      gemm_set_A(g, absorb.p, cols, false);
+      gemm_set_B(g, nxt.d.p, (long long)nxt.m * nxt.r1, false);
+      gemm_set_C(g, nn.d.p, (long long)nxt.m * nxt.r1);
+      gemm(g, c_.stream);
+      x_[k + 1] = std::move(nn);
+      env_step_left(k, true, true);
+    } else {
+      const int zcols = m * zr, kz = std::min(zcols, zl);
+      Core nz = make_core(c_, kz, m, 1, zr);
+      // qr(zeta.reshape(zl, m zr).T); z core = Q^T written directly
+      qr(c_, ctrans(crowmajor(zeta.p, zl, zcols)), MatView{nz.d.p, zcols, kz, 1, zcols}, MatView{});
+      z_[k] = std::move(nz);
+      // x_k = q^T (kq, m, rr)
+      Core nx = make_core(c_, kq, m, 1, rr);
+      copy_view(c_, ctrans(crowmajor(Q.p, rows, kq)), rowmajor(nx.d.p, kq, rows));
+      x_[k] = std::move(nx);
+      // x_{k-1} = x_{k-1} @ absorb^T   ((r0' m') x rl) @ (rl x kq)
+      Core& prv = x_[k - 1];
+      Core np = make_core(c_, prv.r0, prv.m, 1, kq);
+      GemmArgs g;
+      g.M = prv.r0 * prv.m; g.N = kq; g.K = cols;
+      gemm_set_A(g, prv.d.p, cols, false);
+      gemm_set_B(g, absorb.p, cols, true);
+      gemm_set_C(g, np.d.p, kq);
+      gemm(g, c_.stream);
+      x_[k - 1] = std::move(np);
+      env_step_right(k, true, true);
+    }
+  }
+  return est;
+}
+
+// ------------------------------------------------------------------ driver pieces
+void Solver::probe_symmetry() {  // amen.py:249-272
+  const std::vector<int> cd = A_.dims();
+  auto random_vec = [&]() {
+    Train v;
+    for (int k = 0; k < K_; ++k) {
+      const int r0 = k == 0 ? 1 : 2, r1 = k == K_ - 1 ? 1 : 2;
+      Core core = make_core(c_, r0, cd[k], 1, r1);
+      const double* h = draws_.take(core.numel());
+      core.d.upload(h, core.numel());
+      v.cores.push_back(std::move(core));
+    }
+    const double nv = tt_norm(c_, v);
+    if (nv > 0) {
+      Train s = tt_scale_copy(c_, v, 1.0 / nv);
+      return s;
+    }
+    return v;
+  };
+  for (int it = 0; it < 2; ++it) {
+    Train u = random_vec();
+    Train v = random_vec();
+    Train au = tt_apply(c_, A_, u);
+    Train av = tt_apply(c_, A_, v);
+    const double s1 = tt_dot(c_, v, au), s2 = tt_dot(c_, u, av);
+    const double scale = tt_norm(c_, au) + tt_norm(c_, av) + 1e-300;
+    if (std::fabs(s1 - s2) > 1e-6 * scale)
+      throw Error(QTT_ERR_SOLVER,
+                  "operator is not symmetric (<v,Au> != <u,Av> on random probes); assemble the "
+                  "system with the symmetric boundary projection P A P + (I - P) before solving");
+  }
+}
+
+Train Solver::default_x0() {  // amen.py:237-246
+  Train diag;
+  for (auto& a : A_.cores) {
+    Core d = make_core(c_, a.r0, a.m, 1, a.r1);
+    op_core_diag(c_, a.d.p, a.r0, a.m, a.r1, d.d.p);
+    diag.cores.push_back(std::move(d));
+  }
+  Train ones = tt_ones(c_, dims_);
+  double n = 1.0;
+  for (int d : dims_) n *= d;
+  const double mean_diag = tt_dot(c_, diag, ones) / n;
+  if (std::fabs(mean_diag) < 1e-300) return tt_round(c_, f_, 1e-12, 8);
+  const double mean_f = tt_dot(c_, f_, ones) / n;
+  return tt_ones(c_, dims_, mean_f / mean_diag);
+}
+
+std::vector<Core> Solver::init_z() {  // amen.py:275-284
+  std::vector<int> rk(K_ + 1, prm_.enrichment_rank);
+  rk[0] = rk[K_] = 1;
+  for (int k = 1; k < K_; ++k) {
+    // cap = min(prod(dims[:k]), prod(dims[k:])), computed without overflow
+    double left = 1, right = 1;
+    for (int j = 0; j < k; ++j) left *= dims_[j];
+    for (int j = k; j < K_; ++j) right *= dims_[j];
+    const double cap = std::min(left, right);
+    if (cap < rk[k]) rk[k] = (int)cap;
+  }
+  Train t;
+  for (int k = 0; k < K_; ++k) {
+    Core core = make_core(c_, rk[k], dims_[k], 1, rk[k + 1]);
+    const double* h = draws_.take(core.numel());
+    core.d.upload(h, core.numel());
+    t.cores.push_back(std::move(core));
+  }
+  orthogonalize_rl(c_, t);
+  return std::move(t.cores);
+}
+
+Train Solver::run(const Train* x0, AmenResult& res) {
+  nf_ = tt_norm(c_, f_);
+  if (nf_ == 0.0) {
+    res.converged = true;
+    res.sweeps_used = 0;
+    res.final_residual = 0.0;
+    return tt_zero(c_, dims_);
+  }
+  prepare_operator(c_, A_);
+  probe_symmetry();
+  Train start = x0 ? clone(c_, *x0) : default_x0();
+  orthogonalize_rl(c_, start);
+  if (tt_norm(c_, start) == 0.0) {
+    start = tt_ones(c_, dims_, nf_);
+    orthogonalize_rl(c_, start);
+  }
+  x_ = std::move(start.cores);
+  z_ = init_z();
+
+  phi_.resize(K_ + 1);
+  phiz_.resize(K_ + 1);
+  psi_.resize(K_ + 1);
+  psiz_.resize(K_ + 1);
+  for (auto* v : {&phi_, &phiz_}) {
+    (*v)[0] = unit_env(c_);
+    (*v)[K_] = unit_env(c_);
+  }
+  for (auto* v : {&psi_, &psiz_}) {
+    (*v)[0] = unit_env(c_);
+    (*v)[K_] = unit_env(c_);
+  }
+
+  const double tol = prm_.residual_tol;
+  lam_max_ = 0.0;
+  bool converged = false, have_final = false;
+  double final_res = 0.0, best = INFINITY;
+  int strikes = 0, last_check = -10;
+  bool x_envs_valid = false, z_envs_valid = false;
+  for (int sw = 1; sw <= prm_.max_sweeps; ++sw) {
+    sweep_ = sw;
+    const bool forward = (sw % 2 == 1);
+    if (!x_envs_valid || !z_envs_valid) full_prepass(forward, !x_envs_valid, !z_envs_valid);
+    const double est = sweep(forward);
+    x_envs_valid = z_envs_valid = true;
+    c_.stats.sweeps++;
+    std::vector<int> rk{1};
+    for (auto& cc : x_) rk.push_back(cc.r1);
+    res.rank_history.push_back(rk);
+    res.residual_history.push_back(est / nf_);
+    const auto& rh = res.residual_history;
+    const bool cert = est / nf_ <= tol;
+    bool plateau = false;
+    if (prm_.stagnation_strikes > 0 && rh.size() >= 8) {
+      const double a = *std::min_element(rh.end() - 4, rh.end());
+      const double b = *std::min_element(rh.end() - 8, rh.end() - 4);
+      plateau = a > 0.97 * b;
+    }
+    const bool spaced = sw - last_check >= 5;
+    if (!cert && !(plateau && spaced)) continue;
+    Train xcur;
+    xcur.cores.reserve(K_);
+    for (auto& cc : x_) {  // non-owning view is not expressible with DBuf; copy is cheap (cores)
+      Core cp = make_core(c_, cc.r0, cc.m, cc.n, cc.r1);
+      QTT_CUDA(cudaMemcpyAsync(cp.d.p, cc.d.p, cc.numel() * 8, cudaMemcpyDeviceToDevice, c_.stream));
+      xcur.cores.push_back(std::move(cp));
+    }
+    bool gram = false;
+    final_res = residual_norm(c_, A_, xcur, f_, &gram);
+    (gram ? res.certifications_gram : res.certifications_exact)++;
+    have_final = true;
+    if (final_res <= tol) {
+      converged = true;
+      break;
+    }
+    if (!cert && spaced) {
+      if (final_res > 0.97 * best) {
+        strikes++;
+        if (strikes >= prm_.stagnation_strikes) break;
+        z_ = init_z();  // fresh enrichment directions (amen.py:485)
+        z_envs_valid = false;
+      } else {
+        strikes = 0;
+      }
+      last_check = sw;
+    }
+    best = std::min(best, final_res);
+  }
+  res.sweeps_used = (int)res.rank_history.size();
+  Train x;
+  x.cores = std::move(x_);
+  if (!have_final || !converged) {
+    bool gram = false;
+    final_res = residual_norm(c_, A_, x, f_, &gram);
+    (gram ? res.certifications_gram : res.certifications_exact)++;
+    converged = final_res <= tol;
+  }
+  res.converged = converged;
+  res.final_residual = final_res;
+  return x;
+}
+
+}  // namespace
+
+Train amen_solve(Ctx& c, Train& A, const Train& f, const Train* x0, const AmenParams& prm,
+                 DrawStream& draws, AmenResult& res) {
+  Solver s(c, A, f, prm, draws);
+  return s.run(x0, res);
+}
+
+}  // namespace qtt

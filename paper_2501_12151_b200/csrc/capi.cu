@@ -1,16 +1,13 @@
 // extern "C" boundary (include/qtt.h).  Every entry point converts exceptions to
 // status codes and records a thread-local message for qtt_last_error().
+#include <atomic>
 #include <cstring>
 #include <string>
 
 #include "../../include/qtt.h"
+#include "capi_internal.cuh"
 #include "contract.cuh"
 #include "engine.cuh"
-
-struct qtt_ctx {
-  qtt::Ctx impl;
-  explicit qtt_ctx(int dev) : impl(dev) {}
-};
 
 namespace qtt {
 
@@ -26,6 +23,12 @@ Ctx::Ctx(int dev) : device(dev) {
   QTT_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   uint64_t thresh = UINT64_MAX;  // keep freed blocks cached in the pool
   QTT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  QTT_CUDA(cudaMalloc((void**)&red_partial, 1024 * sizeof(double)));
+  QTT_CUDA(cudaMalloc((void**)&red_counter, 64 * sizeof(unsigned)));
+  QTT_CUDA(cudaMemset(red_counter, 0, 64 * sizeof(unsigned)));
+  QTT_CUDA(cudaMalloc((void**)&flags, 64 * sizeof(int)));
+  QTT_CUDA(cudaMemset(flags, 0, 64 * sizeof(int)));
+  QTT_CUDA(cudaMalloc((void**)&scal, 256 * sizeof(double)));
 }
 
 Ctx::~Ctx() {
@@ -34,8 +37,16 @@ Ctx::~Ctx() {
     cudaStreamDestroy(stream);
   }
   if (pinned) cudaFreeHost(pinned);
+  if (red_partial) cudaFree(red_partial);
+  if (red_counter) cudaFree(red_counter);
+  if (flags) cudaFree(flags);
+  if (scal) cudaFree(scal);
   for (auto ev : ev_pool) cudaEventDestroy(ev);
 }
+
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 double* Ctx::host_scalars(size_t n) {
   if (n > pinned_n) {
@@ -51,6 +62,15 @@ double* Ctx::host_scalars(size_t n) {
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+int qtt::capi_guard_store(const char* what, int code) {
+  g_last_error = what;
+  return code;
+}
+
+namespace {
 
 template <class F>
 int guarded(F&& f) {

@@ -1,0 +1,310 @@
+// extern "C" boundary, part 2: device-resident trains, TT algebra, dense
+// factorizations and the AMEn solve (include/qtt.h).
+#include <cmath>
+#include <string>
+
+#include "../../include/qtt.h"
+#include "amen.cuh"
+#include "contract.cuh"
+#include "linalg.cuh"
+#include "capi_internal.cuh"
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return QTT_OK;
+  } catch (const qtt::Error& e) {
+    return qtt::capi_guard_store(e.what(), e.code);
+  } catch (const std::bad_alloc& e) {
+    return qtt::capi_guard_store(e.what(), QTT_ERR_CAPACITY);
+  } catch (const std::exception& e) {
+    return qtt::capi_guard_store(e.what(), QTT_ERR_CUDA);
+  }
+}
+
+qtt::Ctx& C(qtt_ctx* c) {
+  if (!c) throw qtt::Error(QTT_ERR_ARG, "null qtt_ctx");
+  QTT_CUDA(cudaSetDevice(c->impl.device));
+  return c->impl;
+}
+
+const qtt::Train& T(const qtt_train* t) {
+  if (!t) throw qtt::Error(QTT_ERR_ARG, "null qtt_train");
+  return t->t;
+}
+
+void check_chain(const qtt::Train& t) {
+  if (t.cores.empty()) throw qtt::Error(QTT_ERR_SHAPE, "a tensor train needs at least one core");
+  if (t.cores.front().r0 != 1 || t.cores.back().r1 != 1)
+    throw qtt::Error(QTT_ERR_SHAPE, "boundary ranks must be 1");
+  for (size_t k = 0; k + 1 < t.cores.size(); ++k)
+    if (t.cores[k].r1 != t.cores[k + 1].r0)
+      throw qtt::Error(QTT_ERR_SHAPE, "rank mismatch between cores " + std::to_string(k) + " and " +
+                                          std::to_string(k + 1));
+}
+
+qtt_train* wrap(qtt::Train&& t) {
+  auto* h = new qtt_train;
+  h->t = std::move(t);
+  return h;
+}
+
+qtt::DBuf up(const double* h, long long n, cudaStream_t s) {
+  qtt::DBuf b(n, s);
+  b.upload(h, n);
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qtt_train_upload(qtt_ctx* ctx, int order, int core_ndim, const int64_t* shape, const double* data,
+                     qtt_train** out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (order < 1) throw qtt::Error(QTT_ERR_SHAPE, "a tensor train needs at least one core");
+    if (core_ndim != 3 && core_ndim != 4) throw qtt::Error(QTT_ERR_ARG, "core_ndim must be 3 or 4");
+    qtt::Train t;
+    t.is_op = core_ndim == 4;
+    long long off = 0;
+    for (int k = 0; k < order; ++k) {
+      const int64_t* s = shape + (long long)k * core_ndim;
+      for (int d = 0; d < core_ndim; ++d)
+        if (s[d] < 1 || s[d] > (1LL << 31)) throw qtt::Error(QTT_ERR_SHAPE, "invalid core shape");
+      qtt::Core core = core_ndim == 4 ? qtt::make_core(c, (int)s[0], (int)s[1], (int)s[2], (int)s[3])
+                                      : qtt::make_core(c, (int)s[0], (int)s[1], 1, (int)s[2]);
+      core.d.upload(data + off, core.numel());
+      off += core.numel();
+      t.cores.push_back(std::move(core));
+    }
+    check_chain(t);
+    *out = wrap(std::move(t));
+  });
+}
+
+int qtt_train_info(const qtt_train* t, int* order, int* core_ndim, int64_t* numel) {
+  return guarded([&] {
+    const qtt::Train& tr = T(t);
+    if (order) *order = tr.order();
+    if (core_ndim) *core_ndim = tr.is_op ? 4 : 3;
+    if (numel) *numel = tr.numel();
+  });
+}
+
+int qtt_train_shape(const qtt_train* t, int64_t* shape) {
+  return guarded([&] {
+    const qtt::Train& tr = T(t);
+    long long i = 0;
+    for (auto& c : tr.cores) {
+      shape[i++] = c.r0;
+      shape[i++] = c.m;
+      if (tr.is_op) shape[i++] = c.n;
+      shape[i++] = c.r1;
+    }
+  });
+}
+
+int qtt_train_download(qtt_ctx* ctx, const qtt_train* t, double* data) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    long long off = 0;
+    for (auto& core : T(t).cores) {
+      core.d.download(data + off, core.numel());
+      off += core.numel();
+    }
+    c.sync();
+  });
+}
+
+int qtt_train_free(qtt_train* t) {
+  return guarded([&] { delete t; });
+}
+
+int qtt_orthogonalize_rl(qtt_ctx* ctx, const qtt_train* a, qtt_train** out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    qtt::Train g = qtt::clone(c, T(a));
+    qtt::orthogonalize_rl(c, g);
+    c.sync();
+    *out = wrap(std::move(g));
+  });
+}
+
+int qtt_tt_norm(qtt_ctx* ctx, const qtt_train* a, double* out) {
+  return guarded([&] { *out = qtt::tt_norm(C(ctx), T(a)); });
+}
+
+int qtt_tt_dot(qtt_ctx* ctx, const qtt_train* a, const qtt_train* b, double* out) {
+  return guarded([&] {
+    const qtt::Train& ta = T(a);
+    const qtt::Train& tb = T(b);
+    if (ta.order() != tb.order()) throw qtt::Error(QTT_ERR_SHAPE, "mode dims differ");
+    for (int k = 0; k < ta.order(); ++k)
+      if (ta.cores[k].m * ta.cores[k].n != tb.cores[k].m * tb.cores[k].n)
+        throw qtt::Error(QTT_ERR_SHAPE, "mode dims differ");
+    *out = qtt::tt_dot(C(ctx), ta, tb);
+  });
+}
+
+int qtt_tt_round(qtt_ctx* ctx, const qtt_train* a, double rel_tol, int max_rank, qtt_train** out) {
+  return guarded([&] {
+    if (rel_tol < 0) throw qtt::Error(QTT_ERR_ARG, "rel_tolerance must be >= 0");
+    qtt::Ctx& c = C(ctx);
+    qtt::Train r = qtt::tt_round(c, T(a), rel_tol, max_rank);
+    c.sync();
+    *out = wrap(std::move(r));
+  });
+}
+
+int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train** out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& ta = T(A);
+    const qtt::Train& tx = T(x);
+    if (!ta.is_op || tx.is_op || ta.order() != tx.order())
+      throw qtt::Error(QTT_ERR_SHAPE, "operator/vector order mismatch");
+    for (int k = 0; k < ta.order(); ++k)
+      if (ta.cores[k].n != tx.cores[k].m)
+        throw qtt::Error(QTT_ERR_SHAPE, "operator col_dims != vector dims");
+    qtt::Train y = qtt::tt_apply(c, ta, tx);
+    c.sync();
+    *out = wrap(std::move(y));
+  });
+}
+
+int qtt_residual_norm(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, const qtt_train* f,
+                      int exact, double* out, int* used_gram) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    bool gram = false;
+    if (exact) *out = qtt::residual_norm_exact(c, T(A), T(x), T(f));
+    else *out = qtt::residual_norm(c, T(A), T(x), T(f), &gram);
+    if (used_gram) *used_gram = gram ? 1 : 0;
+  });
+}
+
+int qtt_qr(qtt_ctx* ctx, const double* mat, int rows, int cols, double* q, double* r) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (rows < 1 || cols < 1) throw qtt::Error(QTT_ERR_SHAPE, "empty matrix");
+    const int k = std::min(rows, cols);
+    auto dm = up(mat, (long long)rows * cols, c.stream);
+    qtt::DBuf dq((long long)rows * k, c.stream), dr((long long)k * cols, c.stream);
+    qtt::qr(c, qtt::crowmajor(dm.p, rows, cols), qtt::rowmajor(dq.p, rows, k),
+            qtt::rowmajor(dr.p, k, cols));
+    if (q) dq.download(q, dq.n);
+    if (r) dr.download(r, dr.n);
+    c.sync();
+  });
+}
+
+int qtt_svd(qtt_ctx* ctx, const double* mat, int rows, int cols, double* u, double* s, double* vt) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (rows < 1 || cols < 1) throw qtt::Error(QTT_ERR_SHAPE, "empty matrix");
+    const int k = std::min(rows, cols);
+    auto dm = up(mat, (long long)rows * cols, c.stream);
+    qtt::DBuf du((long long)rows * k, c.stream), ds(k, c.stream), dv((long long)k * cols, c.stream);
+    qtt::svd(c, qtt::crowmajor(dm.p, rows, cols), qtt::rowmajor(du.p, rows, k), ds.p,
+             qtt::rowmajor(dv.p, k, cols));
+    if (u) du.download(u, du.n);
+    if (s) ds.download(s, ds.n);
+    if (vt) dv.download(vt, dv.n);
+    c.sync();
+  });
+}
+
+int qtt_rank_for_tolerance(const double* s, int n, double delta, int* out) {
+  return guarded([&] { *out = qtt::rank_for_tolerance(s, n, delta); });
+}
+
+int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const qtt_train* x0,
+                   const qtt_amen_params* prm, const double* draws, int64_t n_draws, qtt_train** x_out,
+                   qtt_amen_report* rep, int32_t* rank_hist, double* res_hist) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& ta = T(A);
+    const qtt::Train& tf = T(f);
+    if (!ta.is_op) throw qtt::Error(QTT_ERR_SHAPE, "A must be a TT linear operator");
+    if (ta.order() != tf.order()) throw qtt::Error(QTT_ERR_SHAPE, "operator/rhs order mismatch");
+    for (int k = 0; k < ta.order(); ++k) {
+      if (ta.cores[k].m != ta.cores[k].n) throw qtt::Error(QTT_ERR_SHAPE, "A is not square");
+      if (ta.cores[k].n != tf.cores[k].m)
+        throw qtt::Error(QTT_ERR_SHAPE, "operator columns do not match f dims");
+    }
+    if (x0) {
+      const qtt::Train& tx = T(x0);
+      if (tx.order() != tf.order()) throw qtt::Error(QTT_ERR_SHAPE, "x0 dims do not match f");
+      for (int k = 0; k < tf.order(); ++k)
+        if (tx.cores[k].m != tf.cores[k].m) throw qtt::Error(QTT_ERR_SHAPE, "x0 dims do not match f");
+    }
+    qtt::AmenParams p;
+    p.residual_tol = prm->residual_tol;
+    p.max_sweeps = prm->max_sweeps;
+    p.enrichment_rank = prm->enrichment_rank;
+    p.local_iterative = prm->local_iterative;
+    p.direct_dim_cap = prm->direct_dim_cap;
+    p.local_iter_cap = prm->local_iter_cap;
+    p.round_tol = prm->round_tol;
+    p.round_max_rank = prm->round_max_rank;
+    p.stagnation_strikes = prm->stagnation_strikes;
+    qtt::DrawStream ds;
+    ds.p = draws;
+    ds.n = n_draws;
+    qtt::AmenResult res;
+    qtt_train* Ah = const_cast<qtt_train*>(A);
+    qtt::Train x = qtt::amen_solve(c, Ah->t, tf, x0 ? &T(x0) : nullptr, p, ds, res);
+    c.sync();
+    rep->converged = res.converged ? 1 : 0;
+    rep->sweeps_used = res.sweeps_used;
+    rep->final_relative_residual = res.final_residual;
+    rep->certifications_gram = res.certifications_gram;
+    rep->certifications_exact = res.certifications_exact;
+    rep->draws_used = ds.pos;
+    const int K = ta.order();
+    for (int s = 0; s < res.sweeps_used && s < p.max_sweeps; ++s) {
+      if (rank_hist)
+        for (int j = 0; j <= K; ++j) rank_hist[(long long)s * (K + 1) + j] = res.rank_history[s][j];
+      if (res_hist) res_hist[s] = res.residual_history[s];
+    }
+    *x_out = wrap(std::move(x));
+  });
+}
+
+int qtt_local_solve(qtt_ctx* ctx, const double* phil, const double* A, const double* phir,
+                    const double* rhs, const double* prev, int rl, int R0, int m, int R1, int rr,
+                    int iterative, int direct_dim_cap, double residual_tol, int iter_cap, double* u,
+                    double* lam, int* iterations) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (rl < 1 || R0 < 1 || m < 1 || R1 < 1 || rr < 1) throw qtt::Error(QTT_ERR_SHAPE, "bad local shape");
+    cudaStream_t s = c.stream;
+    const long long dim = (long long)rl * m * rr;
+    auto dl = up(phil, (long long)rl * R0 * rl, s);
+    auto dA = up(A, (long long)R0 * m * m * R1, s);
+    auto dr = up(phir, (long long)rr * R1 * rr, s);
+    auto db = up(rhs, dim, s);
+    auto dp = up(prev, dim, s);
+    qtt::DBuf Ap((long long)R0 * m * m * R1, s);
+    qtt::permute_op_core(dA.p, R0, m, m, R1, Ap.p, nullptr, s);
+    qtt::LocalSystem L{dl.p, rl, R0, rl, dA.p, Ap.p, R0, m, m, R1, dr.p, rr, R1, rr};
+    qtt::AmenParams p;
+    p.local_iterative = iterative;
+    p.direct_dim_cap = direct_dim_cap;
+    p.residual_tol = residual_tol;
+    p.local_iter_cap = iter_cap;
+    double l = 0;
+    int it = 0;
+    qtt::DBuf du = qtt::solve_local_system(c, L, db.p, dp.p, p, 0, 0, l, it, false);
+    du.download(u, dim);
+    c.sync();
+    if (lam) *lam = l;
+    if (iterations) *iterations = it;
+  });
+}
+
+}  // extern "C"

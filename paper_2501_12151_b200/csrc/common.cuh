@@ -34,8 +34,17 @@ struct Error : public std::runtime_error {
     }                                                                                      \
   } while (0)
 
-#define QTT_CHECK_LAUNCH() QTT_CUDA(cudaGetLastError())
+#define QTT_CHECK_LAUNCH()           \
+  do {                               \
+    QTT_CUDA(cudaGetLastError());    \
+    ::qtt::count_launch();           \
+  } while (0)
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Process-wide count of kernel launches issued by this library (reported as
+// "gpu_launches" by bench.py; every launcher calls count_launch()).
+long long launch_count();
+void count_launch(long long n = 1);
 
 }  // namespace qtt

@@ -132,7 +132,7 @@ long long local_matvec_scratch(int rX, int Ra, int rU, int m, int n, int Rb, int
 
 void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, int m, int n, int Rb,
                   const double* phir, int rY, int rV, const double* v, double* y, double alpha,
-                  double beta, Scratch sc, cudaStream_t s) {
+                  double beta, Scratch sc, cudaStream_t s, const int* skip) {
   double* t1 = take(sc, (long long)rX * Ra * n * rV).p;  // [X][a][n][V]
   double* t2 = take(sc, (long long)rX * m * Rb * rV).p;  // [X][m][b][V]
   {  // t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
@@ -141,6 +141,7 @@ void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, 
     gemm_set_A(g, phil, rU, false);
     gemm_set_B(g, v, (long long)n * rV, false);
     gemm_set_C(g, t1, (long long)n * rV);
+    g.skip = skip;
     gemm(g, s, sc.p, sc.n);
   }
   {  // per X: t2[X][(m,b),V] = Ap[(m,b),(a,n)] @ t1[X][(a,n),V]
@@ -152,6 +153,7 @@ void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, 
     gemm_set_C(g, t2, rV);
     g.c_bs1 = (long long)m * Rb * rV;
     g.batch1 = rX;
+    g.skip = skip;
     gemm(g, s);
   }
   {  // y[(X,m),Y] = alpha * t2[(X,m),(b,V)] @ phir[Y,(b,V)]^T + beta * y
@@ -161,6 +163,7 @@ void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, 
     gemm_set_B(g, phir, (long long)Rb * rV, true);
     gemm_set_C(g, y, rY);
     g.alpha = alpha; g.beta = beta;
+    g.skip = skip;
     gemm(g, s, sc.p, sc.n);
   }
 }

@@ -39,7 +39,7 @@ void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int
 long long local_matvec_scratch(int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV);
 void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, int m, int n, int Rb,
                   const double* phir, int rY, int rV, const double* v, double* y, double alpha,
-                  double beta, Scratch sc, cudaStream_t s);
+                  double beta, Scratch sc, cudaStream_t s, const int* skip = nullptr);
 
 // psi'[U,G] = sum psi[X,F] f[F,m,G] bra[X,m,U]                          (amen.py:120-122)
 void psi_left(const double* psi, int rX, int rF, const double* bra, int m, int rU, const double* f,

@@ -27,6 +27,11 @@ struct Ctx {
   double* pinned = nullptr;
   size_t pinned_n = 0;
   std::vector<cudaEvent_t> ev_pool;
+  // deterministic-reduction scratch (linalg.cu) and small device flags
+  double* red_partial = nullptr;   // 1024 doubles
+  unsigned* red_counter = nullptr; // 1 counter
+  int* flags = nullptr;            // 64 ints (Cholesky info, CG done, ...)
+  double* scal = nullptr;          // 256 device scalars
   explicit Ctx(int dev);
   ~Ctx();
   double* host_scalars(size_t n);

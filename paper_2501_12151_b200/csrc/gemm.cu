@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
   double* sA = smem;
   double* sB = smem + STAGES * BK * LDA;
 
+  if (g.skip != nullptr && *g.skip != 0) return;
+  if (g.lower_only && (int)(blockIdx.x * BN) >= (int)(blockIdx.y * BM + BM)) return;
   int z = blockIdx.z;
   const int split = z % splits;
   z /= splits;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
       const int col = n0 + wn0 + j * 8 + lc * 2;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        if (row < M && col + t < N) {
+        if (row < M && col + t < N && (!g.lower_only || col + t <= row)) {
           double* p = C + (long long)row * g.c_rs + (long long)(col + t) * g.c_cs;
           double v = alpha * acc[i][j][t];
           if (beta != 0.0) v = fma(beta, *p, v);
@@ -256,6 +258,10 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
     return;
   }
   Plan p = plan_for(g);
+  if (g.lower_only || g.skip != nullptr) {
+    p.splits = 1;
+    p.kt_per = cdiv(g.K, 16);
+  }
   if (p.splits > 1 && (ws == nullptr || ws_doubles < (long long)p.splits * g.M * g.N)) {
     p.splits = 1;
     p.kt_per = cdiv(g.K, 16);

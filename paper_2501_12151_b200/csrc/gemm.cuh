@@ -29,6 +29,12 @@ struct GemmArgs {
   long long c_rs = 0, c_cs = 0, c_bs1 = 0, c_bs2 = 0;
   int batch1 = 1, batch2 = 1;
   double alpha = 1.0, beta = 0.0;
+  // Optional device flag: when non-null and *skip != 0 the launch is a no-op
+  // (device-resident CG loops stop without a host round trip).
+  const int* skip = nullptr;
+  // Only tiles touching the lower triangle (row >= col) are computed (SYRK-style
+  // trailing update of the blocked Cholesky); strictly-upper tiles are skipped.
+  bool lower_only = false;
 };
 
 // Row-major helpers: X is (rows x cols) with leading dimension ld.

@@ -1,0 +1,623 @@
+// Dense FP64 kernels of the sweep (see linalg.cuh).
+#include <algorithm>
+#include <cmath>
+
+#include "gemm.cuh"
+#include "linalg.cuh"
+
+namespace qtt {
+namespace {
+
+constexpr int kSmemDoubles = 27 * 1024;  // working sets up to 216 KB stay in shared memory
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum, result broadcast to every thread.  red must hold >= 33 doubles.
+template <int NT>
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < NT / 32 ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// ------------------------------------------------------------------ Householder QR
+// One CTA.  W is the column-major m x n working copy (shared memory when it fits,
+// else global scratch).  tau has k entries.
+template <int NT>
+__global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView Ro, double* gws,
+                                                int use_smem) {
+  extern __shared__ double sm[];
+  __shared__ double red[40];
+  const int m = in.rows, n = in.cols, k = min(m, n);
+  double* W = use_smem ? sm : gws;
+  double* tau = use_smem ? sm + (long long)m * n : gws + (long long)m * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+
+  for (long long e = tid; e < (long long)m * n; e += NT) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    W[e] = in.p[i * in.rs + j * in.cs];
+  }
+  __syncthreads();
+
+  for (int j = 0; j < k; ++j) {
+    double* vj = W + (long long)j * m;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) part += vj[i] * vj[i];
+    const double xnorm2 = block_sum<NT>(part, red);
+    const double alpha = vj[j];
+    double t = 0.0, beta = alpha, scal = 1.0;
+    if (xnorm2 > 0.0) {  // dlarfg
+      beta = -copysign(hypot(alpha, sqrt(xnorm2)), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    if (xnorm2 > 0.0)
+      for (int i = j + 1 + tid; i < m; i += NT) vj[i] *= scal;
+    if (tid == 0) {
+      tau[j] = t;
+      vj[j] = beta;
+    }
+    __syncthreads();
+    if (t != 0.0) {
+      for (int c = j + 1 + warp; c < n; c += NW) {
+        double* wc = W + (long long)c * m;
+        double w = lane == 0 ? wc[j] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w += vj[i] * wc[i];
+        w = warp_sum(w) * t;
+        if (lane == 0) wc[j] -= w;
+        for (int i = j + 1 + lane; i < m; i += 32) wc[i] -= w * vj[i];
+      }
+    }
+    __syncthreads();
+  }
+
+  if (Ro.p) {
+    for (long long e = tid; e < (long long)k * n; e += NT) {
+      const int i = (int)(e % k), c = (int)(e / k);
+      Ro.p[i * Ro.rs + c * Ro.cs] = (i <= c) ? W[(long long)c * m + i] : 0.0;
+    }
+  }
+  if (!Qo.p) return;
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {  // dorg2r, in place on columns 0..k-1
+    double* vj = W + (long long)j * m;
+    const double t = tau[j];
+    if (j < k - 1 && t != 0.0) {
+      for (int c = j + 1 + warp; c < k; c += NW) {
+        double* wc = W + (long long)c * m;
+        double w = lane == 0 ? wc[j] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w += vj[i] * wc[i];
+        w = warp_sum(w) * t;
+        if (lane == 0) wc[j] -= w;
+        for (int i = j + 1 + lane; i < m; i += 32) wc[i] -= w * vj[i];
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += NT) {
+      if (i > j) vj[i] *= -t;
+      else if (i == j) vj[i] = 1.0 - t;
+      else vj[i] = 0.0;
+    }
+    __syncthreads();
+  }
+  for (long long e = tid; e < (long long)m * k; e += NT) {
+    const int i = (int)(e % m), c = (int)(e / m);
+    Qo.p[i * Qo.rs + c * Qo.cs] = W[e];
+  }
+}
+
+// ------------------------------------------------------------------ one-sided Jacobi
+// Orthogonalizes the columns of the column-major m x n matrix W (round-robin
+// parallel ordering, one warp per column pair), accumulating V (n x n).
+// Outputs (sorted by descending norm): U = W/sigma (m x n view), s, Vt (n x n view).
+template <int NT>
+__global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, double* so, MatView Vto,
+                                                    double* gws, int use_smem, double tol) {
+  extern __shared__ double sm[];
+  __shared__ int s_rot;
+  const int m = in.rows, n = in.cols;
+  double* W = use_smem ? sm : gws;                      // m x n, column-major
+  double* V = W + (long long)m * n;                     // n x n, column-major
+  double* sig = V + (long long)n * n;                   // n
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+
+  for (long long e = tid; e < (long long)m * n; e += NT) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    W[e] = in.p[i * in.rs + j * in.cs];
+  }
+  for (long long e = tid; e < (long long)n * n; e += NT) V[e] = (e % n == e / n) ? 1.0 : 0.0;
+  __syncthreads();
+
+  const int P = n + (n & 1);  // players incl. a dummy when n is odd
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < P - 1; ++r) {
+      for (int q = warp; q < P / 2; q += NW) {
+        int a, b;
+        if (q == 0) { a = r; b = P - 1; }
+        else { a = (r + q) % (P - 1); b = (r - q + (P - 1)) % (P - 1); }
+        if (a >= n || b >= n) continue;
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* wa = W + (long long)a * m;
+        double* wb = W + (long long)b * m;
+        double al = 0, be = 0, ga = 0;
+        for (int i = lane; i < m; i += 32) {
+          const double x = wa[i], y = wb[i];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = lane; i < m; i += 32) {
+          const double x = wa[i], y = wb[i];
+          wa[i] = cs * x - sn * y;
+          wb[i] = sn * x + cs * y;
+        }
+        double* va = V + (long long)a * n;
+        double* vb = V + (long long)b * n;
+        for (int i = lane; i < n; i += 32) {
+          const double x = va[i], y = vb[i];
+          va[i] = cs * x - sn * y;
+          vb[i] = sn * x + cs * y;
+        }
+        if (lane == 0) s_rot = 1;
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // column norms
+  for (int c = warp; c < n; c += NW) {
+    const double* wc = W + (long long)c * m;
+    double s2 = 0;
+    for (int i = lane; i < m; i += 32) s2 += wc[i] * wc[i];
+    s2 = warp_sum(s2);
+    if (lane == 0) sig[c] = sqrt(s2);
+  }
+  __syncthreads();
+  // stable descending rank of each column, then scatter
+  for (int c = tid; c < n; c += NT) {
+    const double sc = sig[c];
+    int rank = 0;
+    for (int d = 0; d < n; ++d) {
+      const double sd = sig[d];
+      rank += (sd > sc) || (sd == sc && d < c);
+    }
+    so[rank] = sc;
+    // U column rank = w_c / sigma_c  (unit basis vector when sigma_c == 0)
+    const double inv = sc > 0 ? 1.0 / sc : 0.0;
+    const double* wc = W + (long long)c * m;
+    if (Uo.p)
+      for (int i = 0; i < m; ++i)
+        Uo.p[i * Uo.rs + rank * Uo.cs] = sc > 0 ? wc[i] * inv : (i == rank ? 1.0 : 0.0);
+    if (Vto.p) {
+      const double* vc = V + (long long)c * n;
+      for (int i = 0; i < n; ++i) Vto.p[rank * Vto.rs + i * Vto.cs] = vc[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Cholesky
+constexpr int CB = 64;  // Cholesky block size
+
+// Factor the diagonal block A[j0:j0+nb, j0:j0+nb] in shared memory.
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* A, int dim, long long ld, int j0,
+                                                         int* info) {
+  if (*info != 0) return;
+  __shared__ double a[CB][CB + 1];
+  __shared__ int bad;
+  const int nb = min(CB, dim - j0);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    a[i][j] = A[(j0 + i) * ld + j0 + j];
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double d = a[j][j];
+    if (!(d > 0.0)) {  // dpotrf: non-positive or NaN pivot
+      if (tid == 0) { bad = 1; atomicCAS(info, 0, j0 + j + 1); }
+      __syncthreads();
+      break;
+    }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    if (tid == 0) a[j][j] = ljj;
+    for (int i = j + 1 + tid; i < nb; i += 256) a[i][j] /= ljj;
+    __syncthreads();
+    // trailing update of the block's lower triangle
+    const int rem = nb - j - 1;
+    for (int e = tid; e < rem * rem; e += 256) {
+      const int i = j + 1 + e / rem, c = j + 1 + e % rem;
+      if (c <= i) a[i][c] -= a[i][j] * a[c][j];
+    }
+    __syncthreads();
+  }
+  if (bad) return;
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int i = e / nb, j = e % nb;
+    if (j <= i) A[(j0 + i) * ld + j0 + j] = a[i][j];
+  }
+}
+
+// Panel solve L21 = A21 L11^{-T} for rows j0+nb .. dim-1 (one thread per row).
+__global__ void __launch_bounds__(128) potrf_trsm_kernel(double* A, int dim, long long ld, int j0,
+                                                         const int* info) {
+  if (*info != 0) return;
+  __shared__ double L[CB][CB + 1];
+  const int nb = min(CB, dim - j0);
+  for (int e = threadIdx.x; e < nb * nb; e += 128) {
+    const int i = e / nb, j = e % nb;
+    L[i][j] = (j <= i) ? A[(j0 + i) * ld + j0 + j] : 0.0;
+  }
+  __syncthreads();
+  const int row = j0 + nb + blockIdx.x * 128 + threadIdx.x;
+  if (row >= dim) return;
+  double x[CB];
+  double* a = A + row * ld + j0;
+#pragma unroll
+  for (int j = 0; j < CB; ++j) x[j] = j < nb ? a[j] : 0.0;
+#pragma unroll
+  for (int j = 0; j < CB; ++j) {
+    if (j < nb) {
+      double v = x[j];
+#pragma unroll
+      for (int p = 0; p < j; ++p) v -= x[p] * L[j][p];
+      x[j] = v / L[j][j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CB; ++j)
+    if (j < nb) a[j] = x[j];
+}
+
+// Forward then backward substitution with L (lower, row-major) in one CTA, blocked
+// by 32 rows: each block's 32x32 triangle is solved by one warp, the remaining
+// right-hand side is updated by all warps (GEMV on the panel below/above).
+__global__ void __launch_bounds__(1024) potrs_kernel(const double* L, int dim, long long ld, double* b) {
+  __shared__ double xb[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // forward: L y = b
+  for (int j0 = 0; j0 < dim; j0 += 32) {
+    const int nb = min(32, dim - j0);
+    if (warp == 0) {
+      double v = lane < nb ? b[j0 + lane] : 0.0;
+      for (int j = 0; j < nb; ++j) {
+        const double lij = lane < nb ? L[(j0 + lane) * ld + j0 + j] : 0.0;
+        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(j0 + j) * ld + j0 + j];
+        if (lane == j) v = xj;
+        else if (lane > j) v -= lij * xj;
+      }
+      if (lane < nb) { b[j0 + lane] = v; xb[lane] = v; }
+    }
+    __syncthreads();
+    for (int i = j0 + nb + tid; i < dim; i += 1024) {
+      double s = 0.0;
+      const double* li = L + i * ld + j0;
+      for (int j = 0; j < nb; ++j) s += li[j] * xb[j];
+      b[i] -= s;
+    }
+    __syncthreads();
+  }
+  // backward: L^T x = y
+  for (int j1 = dim; j1 > 0; j1 -= 32) {
+    const int j0 = max(0, j1 - 32), nb = j1 - j0;
+    if (warp == 0) {
+      double v = lane < nb ? b[j0 + lane] : 0.0;
+      for (int j = nb - 1; j >= 0; --j) {
+        // L^T[lane, j] = L[j0+j, j0+lane]
+        const double lji = lane < nb ? L[(j0 + j) * ld + j0 + lane] : 0.0;
+        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(j0 + j) * ld + j0 + j];
+        if (lane == j) v = xj;
+        else if (lane < j) v -= lji * xj;
+      }
+      if (lane < nb) { b[j0 + lane] = v; xb[lane] = v; }
+    }
+    __syncthreads();
+    // b[i] -= sum_j L[j0+j, i] x[j]  for i < j0  (column access: rows j0..j1 of L, coalesced in i)
+    for (int i = tid; i < j0; i += 1024) {
+      double s = 0.0;
+      for (int j = 0; j < nb; ++j) s += L[(j0 + j) * ld + i] * xb[j];
+      b[i] -= s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void row_abs_sum_kernel(const double* A, int dim, long long ld, double* out) {
+  // one warp per row; max over rows via integer atomicMax on non-negative doubles
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= dim) return;
+  const double* a = A + row * ld;
+  double s = 0.0;
+  for (int j = lane; j < dim; j += 32) s += fabs(a[j]);
+  s = warp_sum(s);
+  if (lane == 0) atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(s));
+}
+
+// ------------------------------------------------------------------ reductions
+constexpr int RED_BLOCKS = 296;
+
+template <int MODE>  // 0: dot(a,b)  1: sum(a)  2: sqrt(dot(a,a))
+__global__ void __launch_bounds__(256) reduce_kernel(const double* a, const double* b, long long n,
+                                                     double* partial, unsigned* counter, double* out) {
+  __shared__ double red[40];
+  __shared__ bool last;
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    if (MODE == 0) s += a[i] * b[i];
+    else if (MODE == 1) s += a[i];
+    else s += a[i] * a[i];
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = s;
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += 256) v += ((volatile double*)partial)[i];
+  v = block_sum<256>(v, red);
+  if (threadIdx.x == 0) {
+    *out = MODE == 2 ? sqrt(v) : v;
+    *counter = 0u;
+  }
+}
+
+template <int MODE>
+void reduce(Ctx& c, const double* a, const double* b, long long n, double* out) {
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(RED_BLOCKS, cdiv(n, 256)));
+  reduce_kernel<MODE><<<blocks, 256, 0, c.stream>>>(a, b, n, c.red_partial, c.red_counter, out);
+  QTT_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ elementwise
+__global__ void kron_core_kernel(const double* A, int Ra0, int m, int n, int Ra1, const double* x,
+                                 int rx0, int rx1, double* y) {
+  const long long total = (long long)Ra0 * rx0 * m * Ra1 * rx1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long t = e;
+    const int yy = (int)(t % rx1); t /= rx1;
+    const int b = (int)(t % Ra1); t /= Ra1;
+    const int mm = (int)(t % m); t /= m;
+    const int xx = (int)(t % rx0); t /= rx0;
+    const int a = (int)t;
+    double s = 0.0;
+    for (int nn = 0; nn < n; ++nn)
+      s += A[(((long long)a * m + mm) * n + nn) * Ra1 + b] * x[((long long)xx * n + nn) * rx1 + yy];
+    y[e] = s;
+  }
+}
+
+__global__ void scale_rows_kernel(const double* in, long long ld_in, const double* scale, int rows,
+                                  int cols, double* out, long long ld_out) {
+  const long long total = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    out[i * ld_out + j] = scale[i] * in[i * ld_in + j];
+  }
+}
+
+__global__ void copy_view_kernel(CMatView in, MatView out) {
+  const long long total = (long long)in.rows * in.cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / in.cols), j = (int)(e % in.cols);
+    out.p[i * out.rs + j * out.cs] = in.p[i * in.rs + j * in.cs];
+  }
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    p[e] = v;
+}
+
+__global__ void axpby_kernel(long long n, double a, const double* x, double b, double* y) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    y[e] = a * x[e] + b * y[e];
+}
+
+__global__ void op_core_diag_kernel(const double* A, int R0, int m, int R1, double* d) {
+  const long long total = (long long)R0 * m * R1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(e % R1), mm = (int)((e / R1) % m), a = (int)(e / ((long long)R1 * m));
+    d[e] = A[(((long long)a * m + mm) * m + mm) * R1 + b];
+  }
+}
+
+inline int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 1184)); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ host wrappers
+void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
+  const int m = in.rows, n = in.cols;
+  if (m <= 0 || n <= 0) return;
+  const int k = std::min(m, n);
+  const long long need = (long long)m * n + k;
+  constexpr int NT = 512;
+  c.stats.qr_calls++;
+  if (need <= kSmemDoubles) {
+    static bool attr = false;
+    if (!attr) {
+      QTT_CUDA(cudaFuncSetAttribute(qr_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemDoubles * 8));
+      attr = true;
+    }
+    qr_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, Q, R, nullptr, 1);
+    QTT_CHECK_LAUNCH();
+  } else {
+    DBuf ws(need, c.stream);
+    qr_kernel<NT><<<1, NT, 0, c.stream>>>(in, Q, R, ws.p, 0);
+    QTT_CHECK_LAUNCH();
+  }
+}
+
+static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
+  const int m = in.rows, n = in.cols;
+  const long long need = (long long)m * n + (long long)n * n + n;
+  constexpr int NT = 512;
+  const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
+  if (need <= kSmemDoubles) {
+    static bool attr = false;
+    if (!attr) {
+      QTT_CUDA(cudaFuncSetAttribute(jacobi_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemDoubles * 8));
+      attr = true;
+    }
+    jacobi_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, U, s, Vt, nullptr, 1, tol);
+    QTT_CHECK_LAUNCH();
+  } else {
+    DBuf ws(need, c.stream);
+    jacobi_kernel<NT><<<1, NT, 0, c.stream>>>(in, U, s, Vt, ws.p, 0, tol);
+    QTT_CHECK_LAUNCH();
+  }
+}
+
+void svd(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
+  const int m = in.rows, n = in.cols;
+  if (m <= 0 || n <= 0) return;
+  c.stats.svd_calls++;
+  if (m >= n) {
+    // in = Q R;  R = U_R S V^T  (Jacobi on R)  =>  U = Q U_R
+    DBuf Q((long long)m * n, c.stream), R((long long)n * n, c.stream), UR((long long)n * n, c.stream);
+    qr(c, in, rowmajor(Q.p, m, n), rowmajor(R.p, n, n));
+    jacobi(c, crowmajor(R.p, n, n), rowmajor(UR.p, n, n), s, Vt);
+    if (U.p) {
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = n;
+      gemm_set_A(g, Q.p, n, false);
+      gemm_set_B(g, UR.p, n, false);
+      g.C = U.p; g.c_rs = U.rs; g.c_cs = U.cs;
+      gemm(g, c.stream);
+    }
+  } else {
+    // in^T = Q R (n x m, Q n x m, R m x m);  R = U_R S V_R^T  =>  in = V_R S (Q U_R)^T
+    DBuf Q((long long)n * m, c.stream), R((long long)m * m, c.stream), UR((long long)m * m, c.stream);
+    qr(c, ctrans(in), rowmajor(Q.p, n, m), rowmajor(R.p, m, m));
+    // Jacobi writes U_R and V_R^T; in's U = V_R  ->  pass U transposed as the "Vt" output
+    jacobi(c, crowmajor(R.p, m, m), rowmajor(UR.p, m, m), s, trans(U));
+    if (Vt.p) {  // Vt (m x n) = (Q U_R)^T = U_R^T Q^T
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = m;
+      gemm_set_A(g, UR.p, m, true);
+      gemm_set_B(g, Q.p, m, true);
+      g.C = Vt.p; g.c_rs = Vt.rs; g.c_cs = Vt.cs;
+      gemm(g, c.stream);
+    }
+  }
+}
+
+void potrf_lower(Ctx& c, double* A, int dim, long long ld, int* info) {
+  QTT_CUDA(cudaMemsetAsync(info, 0, sizeof(int), c.stream));
+  for (int j0 = 0; j0 < dim; j0 += CB) {
+    const int nb = std::min(CB, dim - j0);
+    potrf_diag_kernel<<<1, 256, 0, c.stream>>>(A, dim, ld, j0, info);
+    QTT_CHECK_LAUNCH();
+    const int rest = dim - j0 - nb;
+    if (rest <= 0) break;
+    potrf_trsm_kernel<<<cdiv(rest, 128), 128, 0, c.stream>>>(A, dim, ld, j0, info);
+    QTT_CHECK_LAUNCH();
+    GemmArgs g;  // A22 -= L21 L21^T  (lower tiles only)
+    g.M = rest; g.N = rest; g.K = nb;
+    double* L21 = A + (long long)(j0 + nb) * ld + j0;
+    gemm_set_A(g, L21, ld, false);
+    gemm_set_B(g, L21, ld, true);
+    gemm_set_C(g, A + (long long)(j0 + nb) * ld + j0 + nb, ld);
+    g.alpha = -1.0; g.beta = 1.0;
+    g.lower_only = true;
+    g.skip = info;
+    gemm(g, c.stream);
+  }
+  c.stats.chol_solves++;
+}
+
+void potrs_lower(Ctx& c, const double* L, int dim, long long ld, double* b) {
+  potrs_kernel<<<1, 1024, 0, c.stream>>>(L, dim, ld, b);
+  QTT_CHECK_LAUNCH();
+}
+
+void max_abs_row_sum(Ctx& c, const double* A, int dim, long long ld, double* out) {
+  QTT_CUDA(cudaMemsetAsync(out, 0, sizeof(double), c.stream));
+  row_abs_sum_kernel<<<cdiv((long long)dim * 32, 256), 256, 0, c.stream>>>(A, dim, ld, out);
+  QTT_CHECK_LAUNCH();
+}
+
+void dot(Ctx& c, const double* a, const double* b, long long n, double* out) { reduce<0>(c, a, b, n, out); }
+void sum(Ctx& c, const double* a, long long n, double* out) { reduce<1>(c, a, nullptr, n, out); }
+void nrm2(Ctx& c, const double* a, long long n, double* out) { reduce<2>(c, a, nullptr, n, out); }
+
+void read_scalars(Ctx& c, const double* dev, int n, double* host) {
+  double* pin = c.host_scalars(n);
+  QTT_CUDA(cudaMemcpyAsync(pin, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  for (int i = 0; i < n; ++i) host[i] = pin[i];
+}
+
+void kron_core(Ctx& c, const double* A, int Ra0, int m, int n, int Ra1, const double* x, int rx0,
+               int rx1, double* y) {
+  const long long total = (long long)Ra0 * rx0 * m * Ra1 * rx1;
+  kron_core_kernel<<<grid_for(total), 256, 0, c.stream>>>(A, Ra0, m, n, Ra1, x, rx0, rx1, y);
+  QTT_CHECK_LAUNCH();
+}
+
+void scale_rows(Ctx& c, const double* in, long long ld_in, const double* scale, int rows, int cols,
+                double* out, long long ld_out) {
+  scale_rows_kernel<<<grid_for((long long)rows * cols), 256, 0, c.stream>>>(in, ld_in, scale, rows,
+                                                                            cols, out, ld_out);
+  QTT_CHECK_LAUNCH();
+}
+
+void copy_view(Ctx& c, CMatView in, MatView out) {
+  copy_view_kernel<<<grid_for((long long)in.rows * in.cols), 256, 0, c.stream>>>(in, out);
+  QTT_CHECK_LAUNCH();
+}
+
+void fill(Ctx& c, double* p, long long n, double v) {
+  if (n <= 0) return;
+  fill_kernel<<<grid_for(n), 256, 0, c.stream>>>(p, n, v);
+  QTT_CHECK_LAUNCH();
+}
+
+void axpby(Ctx& c, long long n, double a, const double* x, double b, double* y) {
+  axpby_kernel<<<grid_for(n), 256, 0, c.stream>>>(n, a, x, b, y);
+  QTT_CHECK_LAUNCH();
+}
+
+void op_core_diag(Ctx& c, const double* A, int R0, int m, int R1, double* d) {
+  op_core_diag_kernel<<<grid_for((long long)R0 * m * R1), 256, 0, c.stream>>>(A, R0, m, R1, d);
+  QTT_CHECK_LAUNCH();
+}
+
+}  // namespace qtt

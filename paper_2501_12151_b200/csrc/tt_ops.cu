@@ -1,0 +1,409 @@
+// TT algebra on device (tt.py): orthogonalization, norms, dots, rounding, apply,
+// and the residual norm of amen.py:87-99.
+#include <algorithm>
+#include <cmath>
+
+#include "contract.cuh"
+#include "gemm.cuh"
+#include "linalg.cuh"
+#include "train.cuh"
+
+namespace qtt {
+namespace {
+
+// out = [[a, 0], [0, sb*b]] block layout of tt_add (tt.py:308-327) for one core.
+// kind 0: first core (concat along r1); 1: last core (concat along r0); 2: middle (block diag).
+__global__ void blockdiag_core_kernel(const double* a, int ra0, int ra1, const double* b, int rb0,
+                                      int rb1, int mn, double sb, int kind, double* out, int r0,
+                                      int r1) {
+  const long long total = (long long)r0 * mn * r1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e % r1), t = (int)((e / r1) % mn), i = (int)(e / ((long long)r1 * mn));
+    double v = 0.0;
+    if (kind == 0) {
+      v = j < ra1 ? a[(long long)t * ra1 + j] : sb * b[(long long)t * rb1 + (j - ra1)];
+    } else if (kind == 1) {
+      v = i < ra0 ? a[(long long)i * mn + t] : sb * b[(long long)(i - ra0) * mn + t];
+    } else {
+      if (i < ra0 && j < ra1) v = a[((long long)i * mn + t) * ra1 + j];
+      else if (i >= ra0 && j >= ra1) v = sb * b[((long long)(i - ra0) * mn + t) * rb1 + (j - ra1)];
+    }
+    out[e] = v;
+  }
+}
+
+__global__ void permute_op_core_r_kernel(const double* __restrict__ A, int R0, int m, int n, int R1,
+                                         double* __restrict__ Ar) {
+  // Ar[(n, b), (a, m)] = A[a, m, n, b]
+  const long long total = (long long)R0 * m * n * R1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long t = e;
+    const int b = (int)(t % R1); t /= R1;
+    const int nn = (int)(t % n); t /= n;
+    const int mm = (int)(t % m); t /= m;
+    const int a = (int)t;
+    Ar[(((long long)nn * R1 + b) * R0 + a) * m + mm] = A[e];
+  }
+}
+
+inline int grid_for(long long n) {
+  return (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 1184));
+}
+
+double read1(Ctx& c, const double* d) {
+  double h;
+  read_scalars(c, d, 1, &h);
+  return h;
+}
+
+}  // namespace
+
+int rank_for_tolerance(const double* s, int n, double delta) {
+  if (n == 0) return 1;
+  std::vector<double> tail(n);
+  double acc = 0.0;
+  for (int i = n - 1; i >= 0; --i) {  // sequential cumsum from the smallest value (numpy order)
+    acc += s[i] * s[i];
+    tail[i] = std::sqrt(acc);
+  }
+  int r = n;
+  for (int j = n - 1; j >= 1; --j) {
+    if (tail[j] <= delta) r = j;
+    else break;
+  }
+  return std::max(r, 1);
+}
+
+Core make_core(Ctx& c, int r0, int m, int n, int r1) {
+  Core k;
+  k.r0 = r0; k.m = m; k.n = n; k.r1 = r1;
+  k.d.alloc(k.numel(), c.stream);
+  return k;
+}
+
+Train clone(Ctx& c, const Train& t) {
+  Train o;
+  o.is_op = t.is_op;
+  for (auto& k : t.cores) {
+    Core n = make_core(c, k.r0, k.m, k.n, k.r1);
+    QTT_CUDA(cudaMemcpyAsync(n.d.p, k.d.p, k.numel() * 8, cudaMemcpyDeviceToDevice, c.stream));
+    o.cores.push_back(std::move(n));
+  }
+  return o;
+}
+
+void prepare_operator(Ctx& c, Train& A) {
+  if (!A.is_op || A.Ap.size() == A.cores.size()) return;
+  A.Ap.clear();
+  A.Aq.clear();
+  for (auto& k : A.cores) {
+    DBuf ap(k.numel(), c.stream), aq(k.numel(), c.stream);
+    permute_op_core(k.d.p, k.r0, k.m, k.n, k.r1, ap.p, aq.p, c.stream);
+    A.Ap.push_back(std::move(ap));
+    A.Aq.push_back(std::move(aq));
+  }
+}
+
+void orthogonalize_rl(Ctx& c, Train& t) {
+  for (int k = t.order() - 1; k > 0; --k) {
+    Core& ck = t.cores[k];
+    const int r0 = ck.r0, mn = ck.m * ck.n, r1 = ck.r1;
+    const int rows = mn * r1, kq = std::min(rows, r0);
+    Core nk = make_core(c, kq, ck.m, ck.n, r1);
+    DBuf R((long long)kq * r0, c.stream);
+    // QR of the transposed unfolding (mn*r1 x r0); Q^T is written straight into the new core
+    qr(c, CMatView{ck.d.p, rows, r0, 1, rows}, MatView{nk.d.p, rows, kq, 1, rows},
+       rowmajor(R.p, kq, r0));
+    Core& cp = t.cores[k - 1];
+    Core np = make_core(c, cp.r0, cp.m, cp.n, kq);
+    GemmArgs g;  // prev (r0' mn' x r0) @ R^T (r0 x kq)
+    g.M = cp.r0 * cp.m * cp.n; g.N = kq; g.K = r0;
+    gemm_set_A(g, cp.d.p, r0, false);
+    gemm_set_B(g, R.p, r0, true);
+    gemm_set_C(g, np.d.p, kq);
+    gemm(g, c.stream);
+    t.cores[k] = std::move(nk);
+    t.cores[k - 1] = std::move(np);
+  }
+}
+
+double tt_norm(Ctx& c, const Train& t) {
+  if (t.order() == 1) {
+    nrm2(c, t.cores[0].d.p, t.cores[0].numel(), c.scal);
+    return read1(c, c.scal);
+  }
+  Train g = clone(c, t);
+  orthogonalize_rl(c, g);
+  nrm2(c, g.cores[0].d.p, g.cores[0].numel(), c.scal);
+  return read1(c, c.scal);
+}
+
+double tt_dot(Ctx& c, const Train& a, const Train& b) {
+  DBuf w(1, c.stream);
+  fill(c, w.p, 1, 1.0);
+  int ra = 1, rb = 1;
+  for (int k = 0; k < a.order(); ++k) {
+    const Core& ca = a.cores[k];
+    const Core& cb = b.cores[k];
+    const int mode = ca.m * ca.n;
+    DBuf s((long long)ra * mode * cb.r1, c.stream);
+    GemmArgs g;  // s[ra, (n, rb')] = w (ra x rb) @ b_k (rb x n rb')
+    g.M = ra; g.N = mode * cb.r1; g.K = rb;
+    gemm_set_A(g, w.p, rb, false);
+    gemm_set_B(g, cb.d.p, (long long)mode * cb.r1, false);
+    gemm_set_C(g, s.p, (long long)mode * cb.r1);
+    gemm(g, c.stream);
+    DBuf w2((long long)ca.r1 * cb.r1, c.stream);
+    GemmArgs h;  // w' = a_k (ra n x ra')^T @ s (ra n x rb')
+    h.M = ca.r1; h.N = cb.r1; h.K = ra * mode;
+    gemm_set_A(h, ca.d.p, ca.r1, true);
+    gemm_set_B(h, s.p, cb.r1, false);
+    gemm_set_C(h, w2.p, cb.r1);
+    gemm(h, c.stream);
+    w = std::move(w2);
+    ra = ca.r1;
+    rb = cb.r1;
+  }
+  return read1(c, w.p);
+}
+
+Train tt_zero(Ctx& c, const std::vector<int>& dims) {
+  Train o;
+  for (int d : dims) {
+    Core k = make_core(c, 1, d, 1, 1);
+    fill(c, k.d.p, d, 0.0);
+    o.cores.push_back(std::move(k));
+  }
+  return o;
+}
+
+Train tt_ones(Ctx& c, const std::vector<int>& dims, double first_value) {
+  Train o;
+  for (size_t i = 0; i < dims.size(); ++i) {
+    Core k = make_core(c, 1, dims[i], 1, 1);
+    fill(c, k.d.p, dims[i], i == 0 ? first_value : 1.0);
+    o.cores.push_back(std::move(k));
+  }
+  return o;
+}
+
+Train tt_scale_copy(Ctx& c, const Train& a, double s) {
+  Train o = clone(c, a);
+  axpby(c, o.cores[0].numel(), 0.0, o.cores[0].d.p, s, o.cores[0].d.p);
+  return o;
+}
+
+Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
+  const int K = a.order();
+  const std::vector<int> old = a.ranks();
+  bool all_one = true;
+  for (int r : old) all_one = all_one && r == 1;
+  if (K == 1 || all_one) return clone(c, a);
+  Train g = clone(c, a);
+  orthogonalize_rl(c, g);
+  nrm2(c, g.cores[0].d.p, g.cores[0].numel(), c.scal);
+  const double nrm = read1(c, c.scal);
+  if (nrm == 0.0) {
+    Train z;
+    z.is_op = a.is_op;
+    for (auto& k : a.cores) {
+      Core q = make_core(c, 1, k.m, k.n, 1);
+      fill(c, q.d.p, q.numel(), 0.0);
+      z.cores.push_back(std::move(q));
+    }
+    return z;
+  }
+  const double delta = rel_tol * nrm / std::sqrt((double)(K - 1));
+  std::vector<double> hs;
+  for (int k = 0; k < K - 1; ++k) {
+    Core& ck = g.cores[k];
+    const int rows = ck.r0 * ck.m * ck.n, cols = ck.r1, kk = std::min(rows, cols);
+    DBuf U((long long)rows * kk, c.stream), s(kk, c.stream), Vt((long long)kk * cols, c.stream);
+    svd(c, crowmajor(ck.d.p, rows, cols), rowmajor(U.p, rows, kk), s.p, rowmajor(Vt.p, kk, cols));
+    hs.resize(kk);
+    read_scalars(c, s.p, kk, hs.data());
+    int r = rank_for_tolerance(hs.data(), kk, delta);
+    r = std::min(r, old[k + 1]);
+    if (max_rank > 0) r = std::min(r, max_rank);
+    Core nk = make_core(c, ck.r0, ck.m, ck.n, r);
+    copy_view(c, CMatView{U.p, rows, r, kk, 1}, rowmajor(nk.d.p, rows, r));
+    DBuf carry((long long)r * cols, c.stream);
+    scale_rows(c, Vt.p, cols, s.p, r, cols, carry.p, cols);
+    Core& cn = g.cores[k + 1];
+    Core nn = make_core(c, r, cn.m, cn.n, cn.r1);
+    GemmArgs h;  // carry (r x r1) @ next (r1 x mn r1')
+    h.M = r; h.N = cn.m * cn.n * cn.r1; h.K = cols;
+    gemm_set_A(h, carry.p, cols, false);
+    gemm_set_B(h, cn.d.p, (long long)cn.m * cn.n * cn.r1, false);
+    gemm_set_C(h, nn.d.p, (long long)cn.m * cn.n * cn.r1);
+    gemm(h, c.stream);
+    g.cores[k] = std::move(nk);
+    g.cores[k + 1] = std::move(nn);
+  }
+  return g;
+}
+
+Train tt_apply(Ctx& c, const Train& A, const Train& x) {
+  Train y;
+  for (int k = 0; k < A.order(); ++k) {
+    const Core& a = A.cores[k];
+    const Core& v = x.cores[k];
+    Core o = make_core(c, a.r0 * v.r0, a.m, 1, a.r1 * v.r1);
+    kron_core(c, a.d.p, a.r0, a.m, a.n, a.r1, v.d.p, v.r0, v.r1, o.d.p);
+    y.cores.push_back(std::move(o));
+  }
+  return y;
+}
+
+Train tt_sub(Ctx& c, const Train& a, const Train& b) {
+  const int K = a.order();
+  Train o;
+  for (int k = 0; k < K; ++k) {
+    const Core& ca = a.cores[k];
+    const Core& cb = b.cores[k];
+    const int mn = ca.m * ca.n;
+    const double sb = (k == 0) ? -1.0 : 1.0;  // tt_scale multiplies the first core only
+    if (K == 1) {
+      Core n = make_core(c, 1, ca.m, ca.n, 1);
+      QTT_CUDA(cudaMemcpyAsync(n.d.p, ca.d.p, ca.numel() * 8, cudaMemcpyDeviceToDevice, c.stream));
+      axpby(c, n.numel(), -1.0, cb.d.p, 1.0, n.d.p);
+      o.cores.push_back(std::move(n));
+      continue;
+    }
+    const int kind = (k == 0) ? 0 : (k == K - 1 ? 1 : 2);
+    const int r0 = kind == 0 ? 1 : ca.r0 + cb.r0;
+    const int r1 = kind == 1 ? 1 : ca.r1 + cb.r1;
+    Core n = make_core(c, r0, ca.m, ca.n, r1);
+    blockdiag_core_kernel<<<grid_for(n.numel()), 256, 0, c.stream>>>(
+        ca.d.p, ca.r0, ca.r1, cb.d.p, cb.r0, cb.r1, mn, sb, kind, n.d.p, r0, r1);
+    QTT_CHECK_LAUNCH();
+    o.cores.push_back(std::move(n));
+  }
+  return o;
+}
+
+double residual_norm_exact(Ctx& c, const Train& A, const Train& x, const Train& f) {
+  Train y = tt_apply(c, A, x);
+  Train d = tt_sub(c, y, f);
+  const double nr = tt_norm(c, d);
+  const double nf = tt_norm(c, f);
+  return nf > 0 ? nr / nf : nr;
+}
+
+// ||Ax||^2 through a 4-index environment E[X, a, b, Y] (bra x, A, A, ket x) -- the
+// Kronecker structure keeps the cost at 4nR^2r^3 + 4mnR^3r^2 per core instead of the
+// (Rr)^3 of a Gram sweep over the explicit rank-Rr product train.
+static double ax_norm2(Ctx& c, const Train& A, const Train& x) {
+  const int K = A.order();
+  DBuf E(1, c.stream);
+  fill(c, E.p, 1, 1.0);
+  int rX = 1, Ra = 1;  // E dims (rX, Ra, Ra, rX)
+  for (int k = 0; k < K; ++k) {
+    const Core& a = A.cores[k];
+    const Core& v = x.cores[k];
+    const int m = a.m, n = a.n, R1 = a.r1, r1 = v.r1;
+    DBuf Ap(a.numel(), c.stream), Ar(a.numel(), c.stream);
+    permute_op_core(a.d.p, a.r0, m, n, R1, Ap.p, nullptr, c.stream);
+    permute_op_core_r_kernel<<<grid_for(a.numel()), 256, 0, c.stream>>>(a.d.p, a.r0, m, n, R1, Ar.p);
+    QTT_CHECK_LAUNCH();
+    // 1. t1[X,a,b,(n',Y')] = E[(X,a,b),Y] @ x[Y,(n',Y')]
+    DBuf t1((long long)rX * Ra * Ra * n * r1, c.stream);
+    {
+      GemmArgs g;
+      g.M = rX * Ra * Ra; g.N = n * r1; g.K = rX;
+      gemm_set_A(g, E.p, rX, false);
+      gemm_set_B(g, v.d.p, (long long)n * r1, false);
+      gemm_set_C(g, t1.p, (long long)n * r1);
+      gemm(g, c.stream);
+    }
+    // 2. per (X,a): t2[X,a][(m,b'),Y'] = Ap[(m,b'),(b,n')] @ t1[X,a][(b,n'),Y']
+    DBuf t2((long long)rX * Ra * m * R1 * r1, c.stream);
+    {
+      GemmArgs g;
+      g.M = m * R1; g.N = r1; g.K = Ra * n;
+      gemm_set_A(g, Ap.p, (long long)Ra * n, false);
+      gemm_set_B(g, t1.p, r1, false);
+      g.b_bs1 = (long long)Ra * n * r1;
+      gemm_set_C(g, t2.p, r1);
+      g.c_bs1 = (long long)m * R1 * r1;
+      g.batch1 = rX * Ra;
+      gemm(g, c.stream);
+    }
+    t1.release();
+    // 3. per X: t3[X][(n,a'),(b',Y')] = Ar[(n,a'),(a,m)] @ t2[X][(a,m),(b',Y')]
+    DBuf t3((long long)rX * n * R1 * R1 * r1, c.stream);
+    {
+      GemmArgs g;
+      g.M = n * R1; g.N = R1 * r1; g.K = Ra * m;
+      gemm_set_A(g, Ar.p, (long long)Ra * m, false);
+      gemm_set_B(g, t2.p, (long long)R1 * r1, false);
+      g.b_bs1 = (long long)Ra * m * R1 * r1;
+      gemm_set_C(g, t3.p, (long long)R1 * r1);
+      g.c_bs1 = (long long)n * R1 * R1 * r1;
+      g.batch1 = rX;
+      gemm(g, c.stream);
+    }
+    t2.release();
+    // 4. E'[X',(a',b',Y')] = x[(X,n),X']^T @ t3[(X,n),(a',b',Y')]
+    DBuf E2((long long)r1 * R1 * R1 * r1, c.stream);
+    {
+      GemmArgs g;
+      g.M = r1; g.N = R1 * R1 * r1; g.K = rX * n;
+      gemm_set_A(g, v.d.p, r1, true);
+      gemm_set_B(g, t3.p, (long long)R1 * R1 * r1, false);
+      gemm_set_C(g, E2.p, (long long)R1 * R1 * r1);
+      gemm(g, c.stream);
+    }
+    E = std::move(E2);
+    rX = r1;
+    Ra = R1;
+  }
+  return read1(c, E.p);
+}
+
+// <f, A x> through the mixed environment (bra f, A, ket x), reusing env_left.
+static double f_ax(Ctx& c, const Train& A, const Train& x, const Train& f) {
+  DBuf phi(1, c.stream);
+  fill(c, phi.p, 1, 1.0);
+  int rF = 1, Ra = 1, rX = 1;
+  for (int k = 0; k < A.order(); ++k) {
+    const Core& a = A.cores[k];
+    const Core& v = x.cores[k];
+    const Core& fk = f.cores[k];
+    DBuf Ap(a.numel(), c.stream);
+    permute_op_core(a.d.p, a.r0, a.m, a.n, a.r1, Ap.p, nullptr, c.stream);
+    DBuf out((long long)fk.r1 * a.r1 * v.r1, c.stream);
+    const long long need = env_left_scratch(rF, Ra, rX, a.m, a.n, a.r1, v.r1) +
+                           (long long)fk.r1 * a.r1 * v.r1 * 8;
+    DBuf sc(need, c.stream);
+    env_left(phi.p, rF, Ra, rX, fk.d.p, fk.r1, Ap.p, a.m, a.n, a.r1, v.d.p, v.r1, out.p,
+             {sc.p, sc.n}, c.stream);
+    phi = std::move(out);
+    rF = fk.r1; Ra = a.r1; rX = v.r1;
+  }
+  return read1(c, phi.p);
+}
+
+double residual_norm(Ctx& c, const Train& A, const Train& x, const Train& f, bool* used_gram) {
+  c.stats.certifications++;
+  const double nf = tt_norm(c, f);
+  const double aa = ax_norm2(c, A, x);
+  const double fa = f_ax(c, A, x, f);
+  const double ff = tt_dot(c, f, f);
+  const double r2 = aa - 2.0 * fa + ff;
+  const double scale = std::fabs(aa) + 2.0 * std::fabs(fa) + std::fabs(ff);
+  // Accept the Gram value only when it is far above its rounding-error floor
+  // (relative error of r2 <= ~1e-3 even with a 100x error growth); otherwise
+  // fall back to the exact QR-sweep norm of the explicit difference train.
+  if (r2 > 1e5 * 2.220446049250313e-16 * scale) {
+    if (used_gram) *used_gram = true;
+    const double nr = std::sqrt(r2);
+    return nf > 0 ? nr / nf : nr;
+  }
+  if (used_gram) *used_gram = false;
+  return residual_norm_exact(c, A, x, f);
+}
+
+}  // namespace qtt

@@ -1,0 +1,67 @@
+"""GPU end-to-end parity of amen_solve against the reference's own trajectories."""
+import numpy as np
+import pytest
+
+from oracle import qtt_oracle as O
+from tests.golden_io import AMEN_CASES, amen_config, load, train
+from tests.test_oracle_golden import check_amen_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def to_config(d):
+    from paper_2501_12151_b200.amen import AmenConfig
+    from paper_2501_12151_b200.tt import TruncationPolicy
+    c = amen_config(d)
+    rel, cap = c.pop("rounding")
+    return AmenConfig(rounding=TruncationPolicy(rel, cap), **c)
+
+
+@pytest.mark.parametrize("case", AMEN_CASES)
+def test_amen_vs_reference(case):
+    from paper_2501_12151_b200.amen import amen_solve
+    from paper_2501_12151_b200.tt import TensorTrain, TTLinearOperator
+    d = load(case)
+    x0 = TensorTrain(train(d, "x0")) if "x0__n" in d else None
+    x, rep = amen_solve(TTLinearOperator(train(d, "A")), TensorTrain(train(d, "f")), x0, to_config(d))
+    r = {"converged": rep.converged, "sweeps_used": rep.sweeps_used,
+         "final_relative_residual": rep.final_relative_residual,
+         "rank_profile_history": rep.rank_profile_history}
+    check_amen_parity(d, r, O.tt_full(list(x.cores)))
+    assert len(rep.residual_history) == rep.sweeps_used
+
+
+def test_zero_rhs():
+    from paper_2501_12151_b200.amen import amen_solve
+    from paper_2501_12151_b200.tt import tt_identity, tt_norm, tt_zero
+    dims = (4, 4, 4)
+    x, rep = amen_solve(tt_identity(dims), tt_zero(dims))
+    assert rep.converged and rep.sweeps_used == 0 and rep.final_relative_residual == 0.0
+    assert x.ranks == (1,) * 4 and tt_norm(x) == 0.0
+
+
+def test_error_paths():
+    from paper_2501_12151_b200.amen import amen_solve
+    from paper_2501_12151_b200.errors import ShapeMismatchError, SolverError
+    from paper_2501_12151_b200.tt import tt_identity, tt_ones, tt_op_add, tt_op_from_dense, tt_op_scale
+    with pytest.raises(ShapeMismatchError):
+        amen_solve(tt_identity((4, 4)), tt_ones((4, 4, 4)))
+    with pytest.raises(SolverError, match="core"):  # singular local system (test_amen.py:173-179)
+        amen_solve(tt_op_scale(tt_identity((4, 4)), 0.0), tt_ones((4, 4)))
+    # a shift plus 2I is not symmetric (test_amen.py:164-170)
+    A = tt_op_add(tt_op_from_dense(np.eye(16, k=4), (4, 4), (4, 4)), tt_op_scale(tt_identity((4, 4)), 2.0))
+    with pytest.raises(SolverError, match="symmetric"):
+        amen_solve(A, tt_ones((4, 4)))
+
+
+def test_identity_and_scaled():
+    from paper_2501_12151_b200.amen import amen_solve, residual_norm
+    from paper_2501_12151_b200.tt import TensorTrain, tt_identity, tt_ones, tt_op_scale, tt_to_dense
+    rng = np.random.default_rng(7)
+    dims = (2, 4, 4)
+    f = TensorTrain([rng.standard_normal((1, 2, 2)), rng.standard_normal((2, 4, 2)),
+                     rng.standard_normal((2, 4, 1))])
+    x, rep = amen_solve(tt_identity(dims), f)
+    assert rep.converged and residual_norm(tt_identity(dims), x, f) <= 1e-13
+    x, rep = amen_solve(tt_op_scale(tt_identity((4, 4)), 2.0), tt_ones((4, 4)))
+    assert rep.converged and np.allclose(tt_to_dense(x), 0.5, atol=1e-12)

@@ -1,0 +1,149 @@
+"""GPU parity of the dense factorizations (K6/K7), TT algebra (K9/K10, rounding)
+and the local solvers (K4/K5) against the reference fixtures and the oracle."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import qtt_oracle as O
+from tests.golden_io import load, train
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def tt():
+    from paper_2501_12151_b200 import tt as T
+    return T
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 3), (3, 5), (64, 32), (200, 104), (130, 130), (7, 300)])
+def test_qr_matches_numpy(tt, shape):
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    a = rng.standard_normal(shape)
+    q, r = tt._qr(a)
+    qn, rn = np.linalg.qr(a)
+    assert rel(q @ r, a) <= 1e-13
+    # LAPACK dlarfg sign convention reproduced -> factors equal, not just up to signs
+    assert rel(q, qn) <= 1e-12 and rel(r, rn) <= 1e-12
+    k = min(shape)
+    assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-13 * k
+
+
+def test_qr_rank_deficient(tt):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((40, 5)) @ rng.standard_normal((5, 12))
+    q, r = tt._qr(a)
+    assert rel(q @ r, a) <= 1e-13
+    z = np.zeros((6, 4))
+    q, r = tt._qr(z)
+    qn, rn = np.linalg.qr(z)
+    assert np.array_equal(r, rn) and rel(q, qn) == 0.0
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (8, 3), (3, 8), (72, 36), (200, 100), (150, 150), (30, 120)])
+def test_svd_matches_numpy(tt, shape):
+    rng = np.random.default_rng(shape[0] + 1000 * shape[1])
+    a = rng.standard_normal(shape) * np.logspace(0, -10, shape[1])[None, :]
+    u, s, vt = tt._svd(a)
+    sn = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(s - sn)) <= 1e-13 * sn[0]
+    assert rel(u @ np.diag(s) @ vt, a) <= 1e-13
+    k = min(shape)
+    assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-12 * k
+    assert np.linalg.norm(vt @ vt.T - np.eye(k)) <= 1e-12 * k
+
+
+def test_truncated_factor_ranks_vs_reference(tt):
+    """K6: the device SVD + rank rule reproduce the reference's rank decisions."""
+    d = load("factor.npz")
+    for i in range(int(d["tf_count"])):
+        mat = d[f"tf{i}_mat"]
+        rel_tol, cap, dabs = d[f"tf{i}_pol"]
+        u, s, vt = tt._svd(mat)
+        norm = float(np.linalg.norm(s))
+        if norm == 0.0:
+            r = 1
+            qw = np.zeros_like(mat)
+        else:
+            delta = rel_tol * norm
+            if dabs >= 0:
+                delta = min(delta, dabs)
+            r = tt._rank_for_tolerance(s, delta)
+            if cap >= 0:
+                r = min(r, int(cap))
+            r = max(r, 1)
+            qw = u[:, :r] @ (s[:r, None] * vt[:r])
+        assert r == int(d[f"tf{i}_rank"]), i
+        assert np.linalg.norm(qw - d[f"tf{i}_qw"]) <= 1e-12 * max(1.0, np.linalg.norm(d[f"tf{i}_qw"]))
+    for j in range(int(d["rr_count"])):
+        assert tt._rank_for_tolerance(d[f"rr{j}_s"], float(d[f"rr{j}_delta"])) == int(d[f"rr{j}_r"])
+
+
+def test_tt_algebra_vs_reference(tt):
+    d = load("tt_ops.npz")
+    v, w, A = (train(d, n) for n in ("v", "w", "A"))
+    orth = tt._orthogonalize_rl(v)
+    ref = train(d, "v_orth")
+    assert [c.shape for c in orth] == [c.shape for c in ref]
+    for c, r in zip(orth, ref):  # same Householder signs -> same cores
+        assert rel(c, r) <= 1e-12
+    V, W = tt.TensorTrain(v), tt.TensorTrain(w)
+    assert abs(tt.tt_norm(V) - float(d["v_norm"])) <= 1e-13 * float(d["v_norm"])
+    assert abs(tt.tt_dot(V, W) - float(d["vw_dot"])) <= 1e-12 * abs(float(d["vw_dot"]))
+    S = tt.tt_add(V, W)
+    for j in range(4):
+        tol, cap = d[f"round{j}_pol"]
+        out = tt.tt_round(S, tt.TruncationPolicy(float(tol), None if cap < 0 else int(cap)))
+        refj = train(d, f"round{j}")
+        assert [c.shape for c in out.cores] == [c.shape for c in refj], j
+        assert rel(O.tt_full(out.cores), O.tt_full(refj)) <= 1e-12
+    dbl = tt.tt_round(tt.tt_add(V, V))
+    assert [c.shape for c in dbl.cores] == [c.shape for c in train(d, "round_double")]
+    Aop = tt.TTLinearOperator(A)
+    av = tt.tt_apply(Aop, V, None)
+    for c, r in zip(av.cores, train(d, "Av")):
+        assert c.shape == r.shape and rel(c, r) <= 1e-15
+    avr = tt.tt_apply(Aop, V, tt.TruncationPolicy(1e-8))
+    assert [c.shape for c in avr.cores] == [c.shape for c in train(d, "Av_round")]
+    assert rel(O.tt_full(avr.cores), O.tt_full(train(d, "Av_round"))) <= 1e-8
+
+
+def test_residual_norm_vs_reference(tt):
+    from paper_2501_12151_b200.amen import residual_norm
+    d = load("tt_ops.npz")
+    V, W = tt.TensorTrain(train(d, "v")), tt.TensorTrain(train(d, "w"))
+    A = tt.TTLinearOperator(train(d, "A"))
+    r = residual_norm(A, V, W)
+    assert abs(r - float(d["resid_none"])) <= 1e-10 * float(d["resid_none"])
+    r2 = residual_norm(A, V, W, tt.TruncationPolicy(1e-9))
+    assert abs(r2 - float(d["resid_round"])) <= 1e-8 * float(d["resid_round"])
+
+
+def test_local_solve_vs_reference():
+    from paper_2501_12151_b200 import _native as nat
+    d = load("solve_local.npz")
+    phil, A, phir, rhs, prev = (nat.f64(d[k]) for k in ("phil", "Ak", "phir", "rhs", "prev"))
+    rl, R0, _ = phil.shape
+    _, m, _, R1 = A.shape
+    rr = phir.shape[0]
+    ctx = nat.default_context()
+    for iterative, tol, key in [(0, 1e-8, "direct"), (1, 1e-8, "iter_u_1e-08"), (1, 1e-4, "iter_u_0.0001")]:
+        u = np.empty((rl, m, rr))
+        lam, its = ctypes.c_double(), ctypes.c_int()
+        nat.call("qtt_local_solve", ctx.handle, nat.dptr(phil), nat.dptr(A), nat.dptr(phir), nat.dptr(rhs),
+                 nat.dptr(prev), rl, R0, m, R1, rr, iterative, 4096, tol, 400, nat.dptr(u),
+                 ctypes.byref(lam), ctypes.byref(its))
+        if key == "direct":
+            assert rel(u, d["direct_u"]) <= 1e-12
+            assert abs(lam.value - float(d["direct_lam"])) <= 1e-12 * float(d["direct_lam"])
+        else:
+            # not bitwise (summation order): within the CG tolerance of the same recurrence
+            assert rel(u, d[key]) <= max(10 * 0.05 * tol, 1e-11)
+            lam_ref = float(d[key.replace("_u_", "_lam_")])
+            assert abs(lam.value - lam_ref) <= 1e-12 * abs(lam_ref)
