@@ -46,7 +46,8 @@ int qtt_ctx_destroy(qtt_ctx* ctx);
 int qtt_ctx_synchronize(qtt_ctx* ctx);
 /* the context's cudaStream_t, as an opaque pointer (for event timing by the host) */
 void* qtt_ctx_stream(qtt_ctx* ctx);
-/* per-kernel CUDA-event timing of K1/K2 inside solves (off by default) */
+/* per-kernel CUDA-event timing of K1/K2 inside solves (off by default);
+ * qtt_stats.launches is the process-wide count of kernels this library launched */
 int qtt_ctx_set_profiling(qtt_ctx* ctx, int on);
 
 typedef struct {
@@ -56,9 +57,17 @@ typedef struct {
   int64_t env_calls;
   double env_flops, env_ms;
   int64_t cg_iters, cg_solves, chol_solves, svd_calls, qr_calls, sweeps, certifications;
+  double k1_timed_flops, env_timed_flops; /* flops of the event-timed launches (profiling) */
+  /* wall ms per solver phase when profiling: other, direct solve, CG solve, mixed residuals,
+   * SVD, QR, environment updates, certification, env pre-pass, local rhs */
+  double phase_ms[10];
 } qtt_stats;
 int qtt_ctx_get_stats(qtt_ctx* ctx, qtt_stats* out);
 int qtt_ctx_reset_stats(qtt_ctx* ctx);
+/* per-local-solve trace of the last solves: 11 int32 per record
+ * (sweep, core, r_left, mode, r_right, z_left, z_right, R_left, R_right, path 0=direct/1=cg, cg_iters);
+ * *n receives the record count, at most cap records are written */
+int qtt_ctx_trace(qtt_ctx* ctx, int32_t* out, int64_t cap, int64_t* n);
 
 /* ---- interface contractions (amen.py:102-160), host buffers ------------------- */
 /* y[X,m,Y] = phil[X,a,U] x[U,n,V] A[a,m,n,b] phir[Y,b,V]     replaces _local_matvec  amen.py:134 */

@@ -33,7 +33,11 @@ class QttStats(ctypes.Structure):
         ("cg_iters", ctypes.c_int64), ("cg_solves", ctypes.c_int64), ("chol_solves", ctypes.c_int64),
         ("svd_calls", ctypes.c_int64), ("qr_calls", ctypes.c_int64), ("sweeps", ctypes.c_int64),
         ("certifications", ctypes.c_int64),
+        ("k1_timed_flops", ctypes.c_double), ("env_timed_flops", ctypes.c_double),
+        ("phase_ms", ctypes.c_double * 10),
     ]
+
+PHASES = ("other", "direct", "cg", "mixed_res", "svd", "qr", "env", "cert", "prepass", "rhs")
 
 
 # name -> argtypes (restype is int unless listed in _RESTYPES)
@@ -47,6 +51,7 @@ SIGNATURES = {
     "qtt_ctx_set_profiling": [_VP, _I],
     "qtt_ctx_get_stats": [_VP, ctypes.POINTER(QttStats)],
     "qtt_ctx_reset_stats": [_VP],
+    "qtt_ctx_trace": [_VP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "qtt_local_matvec": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
     "qtt_env_left": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
     "qtt_env_right": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
@@ -170,10 +175,23 @@ class Context:
     def stats(self) -> dict:
         s = QttStats()
         call("qtt_ctx_get_stats", self.handle, ctypes.byref(s))
-        return {name: getattr(s, name) for name, _ in QttStats._fields_}
+        out = {name: getattr(s, name) for name, _ in QttStats._fields_ if name != "phase_ms"}
+        out["phase_ms"] = {PHASES[i]: float(s.phase_ms[i]) for i in range(10)}
+        return out
 
     def reset_stats(self):
         call("qtt_ctx_reset_stats", self.handle)
+
+    TRACE_FIELDS = ("sweep", "core", "rl", "m", "rr", "zl", "zr", "R0", "R1", "path", "iters")
+
+    def trace(self) -> np.ndarray:
+        """(n, 11) int32 array of local-solve records since the last reset_stats()."""
+        n = ctypes.c_int64()
+        call("qtt_ctx_trace", self.handle, None, 0, ctypes.byref(n))
+        out = np.zeros((max(n.value, 1), 11), dtype=np.int32)
+        call("qtt_ctx_trace", self.handle, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+             n.value, ctypes.byref(n))
+        return out[: n.value]
 
 
 _default_ctx = {}

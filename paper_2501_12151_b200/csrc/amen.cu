@@ -226,39 +226,13 @@ Env unit_env(Ctx& c) {
   return e;
 }
 
-struct EventTimer {
-  Ctx& c;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
-  size_t used = 0;
-  explicit EventTimer(Ctx& cc) : c(cc) {}
-  ~EventTimer() {
-    for (auto& p : pairs) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
-  }
-  int start() {
-    if (used == pairs.size()) {
-      cudaEvent_t a, b;
-      QTT_CUDA(cudaEventCreate(&a));
-      QTT_CUDA(cudaEventCreate(&b));
-      pairs.push_back({a, b});
-    }
-    QTT_CUDA(cudaEventRecord(pairs[used].first, c.stream));
-    return (int)used++;
-  }
-  void stop(int i) { QTT_CUDA(cudaEventRecord(pairs[i].second, c.stream)); }
-  double ms(int i) {
-    float t = 0;
-    QTT_CUDA(cudaEventElapsedTime(&t, pairs[i].first, pairs[i].second));
-    return t;
-  }
-  void reset() { used = 0; }
-};
+
 
 }  // namespace
 
 DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, const double* prev_p,
                         const AmenParams& prm_, int sweep_, int k, double& lam, int& iters,
                         bool profile) {
-  EventTimer timer_(c_);
   const int m = L.m;
   const long long dim = (long long)L.lb * m * L.rb;
   DBuf mv_scratch;
@@ -327,9 +301,9 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
   const double kflops = local_matvec_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk);
   int* flags = c_.flags;
   if (xany) {  // r = b - A x0
-    int t = profile ? timer_.start() : -1;
+    const int t = c_.prof_begin();
     matvec(u.p, r.p, -1.0, 1.0, nullptr);
-    if (t >= 0) timer_.stop(t);
+    c_.prof_end(t, 0, kflops);
     c_.stats.k1_calls++;
     c_.stats.k1_flops += kflops;
   }
@@ -347,9 +321,10 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     for (int launched = 0; launched < maxiter;) {
       const int nlaunch = std::min(CHUNK, maxiter - launched);
       for (int i = 0; i < nlaunch; ++i) {
-        int t = profile ? timer_.start() : -1;
+        const int t = c_.prof_begin();
         matvec(p.p, q.p, 1.0, 0.0, flags);
-        if (t >= 0) { timer_.stop(t); tidx.push_back(t); }
+        c_.prof_end(t, 0, kflops);
+        tidx.push_back(t);
         cg_alpha_kernel<<<rb, 256, 0, c_.stream>>>(p.p, q.p, dim, c_.red_partial, c_.red_counter, c_.scal,
                                                    flags);
         QTT_CHECK_LAUNCH();
@@ -371,11 +346,9 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
   c_.stats.k1_calls += done_iters;
   c_.stats.k1_flops += kflops * done_iters;
   iters = done_iters;
-  if (profile) {
-    c_.sync();
-    if (xany) c_.stats.k1_ms += timer_.ms(0);
-    for (int i = 0; i < done_iters && i < (int)tidx.size(); ++i) c_.stats.k1_ms += timer_.ms(tidx[i]);
-  }
+  // launches after convergence were no-ops (device skip flag): not K1 work
+  for (int i = done_iters; i < (int)tidx.size(); ++i) c_.prof_discard(tidx[i]);
+  (void)profile;
   return u;
 }
 
@@ -384,7 +357,7 @@ namespace {
 class Solver {
  public:
   Solver(Ctx& c, Train& A, const Train& f, const AmenParams& prm, DrawStream& draws)
-      : c_(c), A_(A), f_(f), prm_(prm), draws_(draws), timer_(c) {
+      : c_(c), A_(A), f_(f), prm_(prm), draws_(draws) {
     K_ = A.order();
     dims_ = f.dims();
   }
@@ -397,7 +370,6 @@ class Solver {
   const Train& f_;
   AmenParams prm_;
   DrawStream& draws_;
-  EventTimer timer_;
   int K_ = 0;
   std::vector<int> dims_;
   std::vector<Core> x_, z_;
@@ -429,19 +401,15 @@ Env Solver::phi_left(const Env& phi, const Core& bra, int k, const Core& ket) {
   Env out;
   out.b = bra.r1; out.o = a.r1; out.k = ket.r1;
   out.d.alloc((long long)out.b * out.o * out.k, c_.stream);
-  DBuf sc(env_left_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r1, ket.r1) +
+  DBuf sc(env_left_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r1, ket.r1, bra.r1) +
               (long long)out.b * out.o * out.k * 4, c_.stream);
-  int t = c_.profiling ? timer_.start() : -1;
+  const double fl = env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r1, bra.r1, ket.r1);
+  const int t = c_.prof_begin();
   env_left(phi.d.p, phi.b, phi.o, phi.k, bra.d.p, bra.r1, A_.Ap[k].p, a.m, a.n, a.r1, ket.d.p, ket.r1,
            out.d.p, {sc.p, sc.n}, c_.stream);
-  if (t >= 0) {
-    timer_.stop(t);
-    c_.sync();
-    c_.stats.env_ms += timer_.ms(t);
-    timer_.reset();
-  }
+  c_.prof_end(t, 1, fl);
   c_.stats.env_calls++;
-  c_.stats.env_flops += env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r1, bra.r1, ket.r1);
+  c_.stats.env_flops += fl;
   return out;
 }
 
@@ -450,19 +418,15 @@ Env Solver::phi_right(const Env& phi, const Core& bra, int k, const Core& ket) {
   Env out;
   out.b = bra.r0; out.o = a.r0; out.k = ket.r0;
   out.d.alloc((long long)out.b * out.o * out.k, c_.stream);
-  DBuf sc(env_right_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r0, ket.r0) +
+  DBuf sc(env_right_scratch(phi.b, phi.o, phi.k, a.m, a.n, a.r0, ket.r0, bra.r0) +
               (long long)out.b * out.o * out.k * 4, c_.stream);
-  int t = c_.profiling ? timer_.start() : -1;
+  const double fl = env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r0, bra.r0, ket.r0);
+  const int t = c_.prof_begin();
   env_right(phi.d.p, phi.b, phi.o, phi.k, bra.d.p, bra.r0, A_.Aq[k].p, a.m, a.n, a.r0, ket.d.p, ket.r0,
             out.d.p, {sc.p, sc.n}, c_.stream);
-  if (t >= 0) {
-    timer_.stop(t);
-    c_.sync();
-    c_.stats.env_ms += timer_.ms(t);
-    timer_.reset();
-  }
+  c_.prof_end(t, 1, fl);
   c_.stats.env_calls++;
-  c_.stats.env_flops += env_flops(phi.b, phi.o, phi.k, a.m, a.n, a.r0, bra.r0, ket.r0);
+  c_.stats.env_flops += fl;
   return out;
 }
 
@@ -510,16 +474,12 @@ DBuf Solver::mixed_res(const Env& psl, int k, const Env& psr, const Env& pl, con
   (void)rl; (void)rr;
   DBuf out = local_rhs_(psl, k, psr);
   const Core& a = A_.cores[k];
-  int t = c_.profiling ? timer_.start() : -1;
+  const double fl = local_matvec_flops(pl.b, pl.o, pl.k, a.m, a.n, a.r1, pr.b, pr.k);
+  const int t = c_.prof_begin();
   matvec(pl, k, pr, u.p, out.p, -1.0, 1.0, nullptr, false);
-  if (t >= 0) {
-    timer_.stop(t);
-    c_.sync();
-    c_.stats.k1_ms += timer_.ms(t);
-    timer_.reset();
-  }
+  c_.prof_end(t, 0, fl);
   c_.stats.k1_calls++;
-  c_.stats.k1_flops += local_matvec_flops(pl.b, pl.o, pl.k, a.m, a.n, a.r1, pr.b, pr.k);
+  c_.stats.k1_flops += fl;
   return out;
 }
 
@@ -529,7 +489,11 @@ DBuf Solver::solve_local(int k, const DBuf& rhs, const Core& prev, double& lam) 
   const Core& a = A_.cores[k];
   LocalSystem L{pl.d.p, pl.b, pl.o, pl.k, a.d.p, A_.Ap[k].p, a.r0, a.m, a.n, a.r1, pr.d.p, pr.b, pr.o, pr.k};
   int iters = 0;
-  return solve_local_system(c_, L, rhs.p, prev.d.p, prm_, sweep_, k, lam, iters, c_.profiling);
+  DBuf u = solve_local_system(c_, L, rhs.p, prev.d.p, prm_, sweep_, k, lam, iters, c_.profiling);
+  const long long dim = (long long)pl.b * a.m * pr.b;
+  const int path = (!prm_.local_iterative && dim <= prm_.direct_dim_cap) ? 0 : 1;
+  c_.trace.push_back({sweep_, k, pl.b, a.m, pr.b, phiz_[k].b, phiz_[k + 1].b, a.r0, a.r1, path, iters});
+  return u;
 }
 
 // ------------------------------------------------------------------ env plumbing
@@ -575,7 +539,9 @@ double Solver::sweep(bool forward) {
     const int rl = x_[k].r0, m = x_[k].m, rr = x_[k].r1;
     DBuf rhs = local_rhs_(psi_[k], k, psi_[k + 1]);
     double lam = 0.0;
+    c_.phase((!prm_.local_iterative && (long long)rl * m * rr <= prm_.direct_dim_cap) ? PH_DIRECT : PH_CG);
     DBuf u = solve_local(k, rhs, x_[k], lam);
+    c_.phase(PH_MIXED);
     lam_max_ = std::max(lam_max_, lam);
     const bool have_dabs = K_ > 1 && lam_max_ > 0;
     const double dabs = have_dabs ? prm_.residual_tol * nf_ / (lam_max_ * std::sqrt((double)(K_ - 1))) : 0.0;
@@ -615,6 +581,7 @@ double Solver::sweep(bool forward) {
     }
     const int kk = std::min(rows, cols);
     DBuf U((long long)rows * kk, c_.stream), s(kk, c_.stream), Vt((long long)kk * cols, c_.stream);
+    c_.phase(PH_SVD);
     svd(c_, uview, rowmajor(U.p, rows, kk), s.p, rowmajor(Vt.p, kk, cols));
     std::vector<double> hs(kk);
     read_scalars(c_, s.p, kk, hs.data());
@@ -643,6 +610,7 @@ double Solver::sweep(bool forward) {
     QTT_CHECK_LAUNCH();
     const int kq = std::min(rows, acols);
     DBuf Q((long long)rows * kq, c_.stream), R((long long)kq * acols, c_.stream);
+    c_.phase(PH_QR);
     qr(c_, crowmajor(aug.p, rows, acols), rowmajor(Q.p, rows, kq), rowmajor(R.p, kq, acols));
     // absorb = R[:, :r] @ w   (kq x cols)
     DBuf absorb((long long)kq * cols, c_.stream);
@@ -674,7 +642,9 @@ double Solver::sweep(bool forward) {
       gemm_set_C(g, nn.d.p, (long long)nxt.m * nxt.r1);
       gemm(g, c_.stream);
       x_[k + 1] = std::move(nn);
+      c_.phase(PH_ENV);
       env_step_left(k, true, true);
+      c_.phase(PH_RHS);
     } else {
       const int zcols = m * zr, kz = std::min(zcols, zl);
       Core nz = make_core(c_, kz, m, 1, zr);
@@ -695,7 +665,9 @@ double Solver::sweep(bool forward) {
       gemm_set_C(g, np.d.p, kq);
       gemm(g, c_.stream);
       x_[k - 1] = std::move(np);
+      c_.phase(PH_ENV);
       env_step_right(k, true, true);
+      c_.phase(PH_RHS);
     }
   }
   return est;
@@ -813,10 +785,13 @@ Train Solver::run(const Train* x0, AmenResult& res) {
   for (int sw = 1; sw <= prm_.max_sweeps; ++sw) {
     sweep_ = sw;
     const bool forward = (sw % 2 == 1);
+    c_.phase(PH_PREPASS);
     if (!x_envs_valid || !z_envs_valid) full_prepass(forward, !x_envs_valid, !z_envs_valid);
+    c_.phase(PH_RHS);
     const double est = sweep(forward);
     x_envs_valid = z_envs_valid = true;
     c_.stats.sweeps++;
+    c_.prof_flush();
     std::vector<int> rk{1};
     for (auto& cc : x_) rk.push_back(cc.r1);
     res.rank_history.push_back(rk);
@@ -839,7 +814,9 @@ Train Solver::run(const Train* x0, AmenResult& res) {
       xcur.cores.push_back(std::move(cp));
     }
     bool gram = false;
+    c_.phase(PH_CERT);
     final_res = residual_norm(c_, A_, xcur, f_, &gram);
+    c_.phase(PH_OTHER);
     (gram ? res.certifications_gram : res.certifications_exact)++;
     have_final = true;
     if (final_res <= tol) {
@@ -860,6 +837,7 @@ Train Solver::run(const Train* x0, AmenResult& res) {
     best = std::min(best, final_res);
   }
   res.sweeps_used = (int)res.rank_history.size();
+  c_.prof_flush();
   Train x;
   x.cores = std::move(x_);
   if (!have_final || !converged) {

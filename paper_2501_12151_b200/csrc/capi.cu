@@ -48,6 +48,30 @@ static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
 void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+void Ctx::phase(int ph) {
+  if (!profiling) return;
+  sync();
+  const double t = std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now().time_since_epoch()).count();
+  if (phase_t0 >= 0) stats.phase_ms[phase_cur] += t - phase_t0;
+  phase_t0 = t;
+  phase_cur = ph;
+}
+
+void Ctx::prof_flush() {
+  if (prof.pending.empty()) return;
+  sync();
+  for (auto& r : prof.pending) {
+    if (!r.keep) continue;
+    float ms = 0;
+    QTT_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    if (r.kind == 0) { stats.k1_ms += ms; stats.k1_timed_flops += r.flops; }
+    else { stats.env_ms += ms; stats.env_timed_flops += r.flops; }
+  }
+  prof.pending.clear();
+  prof.next = 0;
+}
+
 double* Ctx::host_scalars(size_t n) {
   if (n > pinned_n) {
     if (pinned) QTT_CUDA(cudaFreeHost(pinned));
@@ -158,6 +182,10 @@ int qtt_ctx_get_stats(qtt_ctx* ctx, qtt_stats* o) {
     o->env_calls = s.env_calls;
     o->env_flops = s.env_flops;
     o->env_ms = s.env_ms;
+    o->k1_timed_flops = s.k1_timed_flops;
+    o->env_timed_flops = s.env_timed_flops;
+    o->launches = qtt::launch_count();
+    for (int i = 0; i < 10; ++i) o->phase_ms[i] = s.phase_ms[i];
     o->cg_iters = s.cg_iters;
     o->cg_solves = s.cg_solves;
     o->chol_solves = s.chol_solves;
@@ -172,8 +200,24 @@ int qtt_ctx_reset_stats(qtt_ctx* ctx) {
   return guarded([&] {
     check_ctx(ctx);
     ctx->impl.stats = qtt::Stats();
+    ctx->impl.trace.clear();
   });
 }
+
+int qtt_ctx_trace(qtt_ctx* ctx, int32_t* out, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    check_ctx(ctx);
+    const auto& t = ctx->impl.trace;
+    *n = (int64_t)t.size();
+    const int64_t k = std::min<int64_t>(cap, (int64_t)t.size());
+    for (int64_t i = 0; i < k; ++i) {
+      const auto& r = t[i];
+      const int32_t v[11] = {r.sweep, r.core, r.rl, r.m, r.rr, r.zl, r.zr, r.R0, r.R1, r.path, r.iters};
+      for (int j = 0; j < 11; ++j) out[i * 11 + j] = v[j];
+    }
+  });
+}
+
 
 int qtt_local_matvec(qtt_ctx* ctx, const double* phil, const double* A, const double* phir,
                      const double* x, int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV,
@@ -210,7 +254,7 @@ int qtt_env_left(qtt_ctx* ctx, const double* phi, const double* bra, const doubl
     auto dket = up(ket, prod({rY, n, rZ}), s);
     qtt::DBuf Ap(prod({RA, m, n, RB}), s), dout(prod({rU, RB, rZ}), s);
     qtt::permute_op_core(dA.p, RA, m, n, RB, Ap.p, nullptr, s);
-    long long need = qtt::env_left_scratch(rX, RA, rY, m, n, RB, rZ);
+    long long need = qtt::env_left_scratch(rX, RA, rY, m, n, RB, rZ, rU);
     qtt::DBuf sc(need + prod({rU, RB * rZ, 64}), s);
     qtt::env_left(dphi.p, rX, RA, rY, dbra.p, rU, Ap.p, m, n, RB, dket.p, rZ, dout.p, {sc.p, sc.n}, s);
     dout.download(out, dout.n);
@@ -231,7 +275,7 @@ int qtt_env_right(qtt_ctx* ctx, const double* phi, const double* bra, const doub
     auto dket = up(ket, prod({rY, n, rZ}), s);
     qtt::DBuf Aq(prod({Ra, m, n, RA}), s), dout(prod({rB, Ra, rY}), s);
     qtt::permute_op_core(dA.p, Ra, m, n, RA, nullptr, Aq.p, s);
-    long long need = qtt::env_right_scratch(rX, RA, rZ, m, n, Ra, rY);
+    long long need = qtt::env_right_scratch(rX, RA, rZ, m, n, Ra, rY, rB);
     qtt::DBuf sc(need + prod({rB, Ra * rY, 64}), s);
     qtt::env_right(dphi.p, rX, RA, rZ, dbra.p, rB, Aq.p, m, n, Ra, dket.p, rY, dout.p, {sc.p, sc.n}, s);
     dout.download(out, dout.n);

@@ -23,6 +23,13 @@ __global__ void permute_op_core_kernel(const double* __restrict__ A, int R0, int
   }
 }
 
+// split-K workspace a plain M x N x K product may ask for (gemm.cu plan)
+long long splitk_ws(int M, int N, int K) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  return gemm_workspace_hint(g);
+}
+
 inline Scratch take(Scratch& sc, long long n) {
   if (n > sc.n) throw Error(QTT_ERR_ARG, "contraction scratch too small");
   Scratch out{sc.p, n};
@@ -42,9 +49,9 @@ void permute_op_core(const double* A, int R0, int m, int n, int R1, double* Ap, 
 }
 
 // ---------------------------------------------------------------- left environment
-long long env_left_scratch(int rX, int RA, int rY, int m, int n, int RB, int rZ) {
-  (void)rY;
-  return (long long)rX * RA * n * rZ + (long long)rX * m * RB * rZ;
+long long env_left_scratch(int rX, int RA, int rY, int m, int n, int RB, int rZ, int rU) {
+  return (long long)rX * RA * n * rZ + (long long)rX * m * RB * rZ +
+         std::max(splitk_ws(rX * RA, n * rZ, rY), splitk_ws(rU, RB * rZ, rX * m));
 }
 
 void env_left(const double* phi, int rX, int RA, int rY, const double* bra, int rU,
@@ -82,9 +89,9 @@ void env_left(const double* phi, int rX, int RA, int rY, const double* bra, int 
 }
 
 // ---------------------------------------------------------------- right environment
-long long env_right_scratch(int rX, int RA, int rZ, int m, int n, int Ra, int rY) {
-  (void)rZ;
-  return (long long)rX * RA * n * rY + (long long)m * rX * Ra * rY;
+long long env_right_scratch(int rX, int RA, int rZ, int m, int n, int Ra, int rY, int rB) {
+  return (long long)rX * RA * n * rY + (long long)m * rX * Ra * rY +
+         splitk_ws(rB, Ra * rY, m * rX);
 }
 
 void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int rB,
@@ -126,8 +133,8 @@ void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int
 
 // ---------------------------------------------------------------- local matvec
 long long local_matvec_scratch(int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV) {
-  (void)rU; (void)rY;
-  return (long long)rX * Ra * n * rV + (long long)rX * m * Rb * rV;
+  return (long long)rX * Ra * n * rV + (long long)rX * m * Rb * rV +
+         std::max(splitk_ws(rX * Ra, n * rV, rU), splitk_ws(rX * m, rY, Rb * rV));
 }
 
 void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, int m, int n, int Rb,

@@ -17,6 +17,7 @@ struct Scratch {
   long long n = 0;
 };
 
+// Scratch sizes below include the deterministic split-K workspace of the long-K steps.
 // Permuted operator-core views (built by permute_op_core):
 //   Ap[(m,B),(A,n)] = A[A,m,n,B]   -- left env step and local matvec
 //   Aq[(m,a),(A,n)] = A[a,m,n,A]   -- right env step  (same as Ap with R0/R1 roles swapped)
@@ -24,13 +25,13 @@ void permute_op_core(const double* A, int R0, int m, int n, int R1, double* Ap, 
                      cudaStream_t s);
 
 // phi'[U,B,Z] = sum phi[X,A,Y] ket[Y,n,Z] A[A,m,n,B] bra[X,m,U]        (amen.py:108-111)
-long long env_left_scratch(int rX, int RA, int rY, int m, int n, int RB, int rZ);
+long long env_left_scratch(int rX, int RA, int rY, int m, int n, int RB, int rZ, int rU);
 void env_left(const double* phi, int rX, int RA, int rY, const double* bra, int rU,
               const double* Ap, int m, int n, int RB, const double* ket, int rZ, double* out,
               Scratch sc, cudaStream_t s);
 
 // phi'[B,a,Y] = sum phi[X,A,Z] ket[Y,n,Z] A[a,m,n,A] bra[B,m,X]        (amen.py:114-117)
-long long env_right_scratch(int rX, int RA, int rZ, int m, int n, int Ra, int rY);
+long long env_right_scratch(int rX, int RA, int rZ, int m, int n, int Ra, int rY, int rB);
 void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int rB,
                const double* Aq, int m, int n, int Ra, const double* ket, int rY, double* out,
                Scratch sc, cudaStream_t s);

@@ -1,6 +1,7 @@
 // Engine context: one CUDA stream + a stream-ordered memory pool per context
 // (re-entrant per handle, no global mutable state; SURVEY.md 8b "Threading").
 #pragma once
+#include <chrono>
 #include <vector>
 
 #include "common.cuh"
@@ -10,16 +11,50 @@ namespace qtt {
 struct Stats {
   long long launches = 0;       // kernel launches issued by this engine (all kinds)
   long long k1_calls = 0;       // local matvec (K1) invocations
-  double k1_flops = 0, k1_ms = 0;
+  double k1_flops = 0, k1_ms = 0, k1_timed_flops = 0;
   long long env_calls = 0;      // environment updates (K2)
-  double env_flops = 0, env_ms = 0;
+  double env_flops = 0, env_ms = 0, env_timed_flops = 0;
   long long cg_iters = 0, cg_solves = 0, chol_solves = 0;
   long long svd_calls = 0, qr_calls = 0;
   long long sweeps = 0, certifications = 0;
+  // wall time per solver phase (profiling mode syncs at phase boundaries)
+  double phase_ms[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+};
+enum Phase { PH_OTHER = 0, PH_DIRECT, PH_CG, PH_MIXED, PH_SVD, PH_QR, PH_ENV, PH_CERT, PH_PREPASS, PH_RHS };
+
+// Deferred CUDA-event timing of the contraction kernels (no host sync at record
+// time; pending pairs are resolved at the solver's existing sync points).
+struct Profiler {
+  struct Rec {
+    cudaEvent_t a, b;
+    int kind;       // 0: K1 local matvec, 1: K2 environment update
+    double flops;
+    bool keep;
+  };
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  std::vector<Rec> pending;
+  cudaEvent_t get() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      QTT_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  ~Profiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// One local solve of a sweep (for the CPU-baseline cost model and diagnostics).
+struct TraceRec {
+  int sweep, core, rl, m, rr, zl, zr, R0, R1, path /*0 direct, 1 cg*/, iters;
 };
 
 struct Ctx {
   int device = 0;
+  std::vector<TraceRec> trace;
   cudaStream_t stream = nullptr;
   bool profiling = false;
   Stats stats;
@@ -32,8 +67,32 @@ struct Ctx {
   unsigned* red_counter = nullptr; // 1 counter
   int* flags = nullptr;            // 64 ints (Cholesky info, CG done, ...)
   double* scal = nullptr;          // 256 device scalars
+  Profiler prof;
   explicit Ctx(int dev);
   ~Ctx();
+  // profiling helpers (no-ops unless profiling): begin returns a record id or -1
+  int prof_begin() {
+    if (!profiling) return -1;
+    Profiler::Rec r{prof.get(), prof.get(), 0, 0.0, true};
+    QTT_CUDA(cudaEventRecord(r.a, stream));
+    prof.pending.push_back(r);
+    return (int)prof.pending.size() - 1;
+  }
+  void prof_end(int id, int kind, double flops) {
+    if (id < 0) return;
+    auto& r = prof.pending[id];
+    QTT_CUDA(cudaEventRecord(r.b, stream));
+    r.kind = kind;
+    r.flops = flops;
+  }
+  void prof_discard(int id) {
+    if (id >= 0) prof.pending[id].keep = false;
+  }
+  // resolve pending records (synchronizes the stream)
+  void prof_flush();
+  int phase_cur = 0;
+  double phase_t0 = -1;
+  void phase(int ph);
   double* host_scalars(size_t n);
   void sync() { QTT_CUDA(cudaStreamSynchronize(stream)); }
 };

@@ -177,7 +177,9 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
 }
 
 __global__ void splitk_reduce(const double* __restrict__ ws, int splits, int M, int N, double* C,
-                              long long c_rs, long long c_cs, double alpha, double beta) {
+                              long long c_rs, long long c_cs, double alpha, double beta,
+                              const int* skip) {
+  if (skip != nullptr && *skip != 0) return;
   const long long total = (long long)M * N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -252,13 +254,13 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
     for (int b2 = 0; b2 < g.batch2; ++b2)
       for (int b1 = 0; b1 < g.batch1; ++b1) {
         double* C = g.C + b1 * g.c_bs1 + b2 * g.c_bs2;
-        splitk_reduce<<<cdiv(total, 256), 256, 0, s>>>(nullptr, 0, g.M, g.N, C, g.c_rs, g.c_cs, 0.0, g.beta);
+        splitk_reduce<<<cdiv(total, 256), 256, 0, s>>>(nullptr, 0, g.M, g.N, C, g.c_rs, g.c_cs, 0.0, g.beta, g.skip);
         QTT_CHECK_LAUNCH();
       }
     return;
   }
   Plan p = plan_for(g);
-  if (g.lower_only || g.skip != nullptr) {
+  if (g.lower_only) {
     p.splits = 1;
     p.kt_per = cdiv(g.K, 16);
   }
@@ -274,7 +276,7 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
   if (p.splits > 1) {
     const long long total = (long long)g.M * g.N;
     int blocks = (int)std::min<long long>(cdiv(total, 256), 4 * kSMs);
-    splitk_reduce<<<blocks, 256, 0, s>>>(ws, p.splits, g.M, g.N, g.C, g.c_rs, g.c_cs, g.alpha, g.beta);
+    splitk_reduce<<<blocks, 256, 0, s>>>(ws, p.splits, g.M, g.N, g.C, g.c_rs, g.c_cs, g.alpha, g.beta, g.skip);
     QTT_CHECK_LAUNCH();
   }
 }

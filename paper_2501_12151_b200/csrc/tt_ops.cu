@@ -375,7 +375,7 @@ static double f_ax(Ctx& c, const Train& A, const Train& x, const Train& f) {
     DBuf Ap(a.numel(), c.stream);
     permute_op_core(a.d.p, a.r0, a.m, a.n, a.r1, Ap.p, nullptr, c.stream);
     DBuf out((long long)fk.r1 * a.r1 * v.r1, c.stream);
-    const long long need = env_left_scratch(rF, Ra, rX, a.m, a.n, a.r1, v.r1) +
+    const long long need = env_left_scratch(rF, Ra, rX, a.m, a.n, a.r1, v.r1, fk.r1) +
                            (long long)fk.r1 * a.r1 * v.r1 * 8;
     DBuf sc(need, c.stream);
     env_left(phi.p, rF, Ra, rX, fk.d.p, fk.r1, Ap.p, a.m, a.n, a.r1, v.d.p, v.r1, out.p,
