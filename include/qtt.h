@@ -46,7 +46,8 @@ int qtt_ctx_destroy(qtt_ctx* ctx);
 int qtt_ctx_synchronize(qtt_ctx* ctx);
 /* the context's cudaStream_t, as an opaque pointer (for event timing by the host) */
 void* qtt_ctx_stream(qtt_ctx* ctx);
-/* per-kernel CUDA-event timing of K1/K2 inside solves (off by default);
+/* on & 1: per-kernel CUDA-event timing of K1/K2 inside solves (deferred, no syncs);
+ * on & 2: per-phase wall timing (synchronizes at phase boundaries); off by default;
  * qtt_stats.launches is the process-wide count of kernels this library launched */
 int qtt_ctx_set_profiling(qtt_ctx* ctx, int on);
 
@@ -63,6 +64,10 @@ typedef struct {
   double phase_ms[10];
 } qtt_stats;
 int qtt_ctx_get_stats(qtt_ctx* ctx, qtt_stats* out);
+/* write 256 MiB of scratch on the context stream (evicts the 126 MB L2 between timed steps) */
+int qtt_ctx_flush_l2(qtt_ctx* ctx);
+/* process-wide number of kernels this library has launched */
+int64_t qtt_launch_count(void);
 int qtt_ctx_reset_stats(qtt_ctx* ctx);
 /* per-local-solve trace of the last solves: 11 int32 per record
  * (sweep, core, r_left, mode, r_right, z_left, z_right, R_left, R_right, path 0=direct/1=cg, cg_iters);
@@ -139,7 +144,7 @@ int qtt_rank_for_tolerance(const double* s, int n, double delta, int* out);  /* 
 int qtt_local_solve(qtt_ctx* ctx, const double* phil, const double* A, const double* phir,
                     const double* rhs, const double* prev, int rl, int R0, int m, int R1, int rr,
                     int iterative, int direct_dim_cap, double residual_tol, int iter_cap,
-                    double* u, double* lam, int* iterations);
+                    int fused_cg, double* u, double* lam, int* iterations);
 
 /* ---- the solve (amen.py:394-510) --------------------------------------------- */
 typedef struct {
@@ -152,6 +157,7 @@ typedef struct {
   double round_tol;       /* rounding.rel_tolerance      (amen.py:59) */
   int round_max_rank;     /* rounding.max_rank, <= 0: None */
   int stagnation_strikes; /* (amen.py:64) */
+  int fused_cg;           /* 1: persistent cooperative CG kernel per local solve; 0: per-step launches */
 } qtt_amen_params;
 
 typedef struct {

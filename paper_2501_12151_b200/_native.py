@@ -51,6 +51,8 @@ SIGNATURES = {
     "qtt_ctx_set_profiling": [_VP, _I],
     "qtt_ctx_get_stats": [_VP, ctypes.POINTER(QttStats)],
     "qtt_ctx_reset_stats": [_VP],
+    "qtt_ctx_flush_l2": [_VP],
+    "qtt_launch_count": [],
     "qtt_ctx_trace": [_VP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
     "qtt_local_matvec": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
     "qtt_env_left": [_VP, _P, _P, _P, _P] + [_I] * 8 + [_P],
@@ -75,7 +77,7 @@ SIGNATURES = {
     "qtt_qr": [_VP, _P, _I, _I, _P, _P],
     "qtt_svd": [_VP, _P, _I, _I, _P, _P, _P],
     "qtt_rank_for_tolerance": [_P, _I, ctypes.c_double, ctypes.POINTER(_I)],
-    "qtt_local_solve": [_VP, _P, _P, _P, _P, _P] + [_I] * 7 + [ctypes.c_double, _I, _P, _P,
+    "qtt_local_solve": [_VP, _P, _P, _P, _P, _P] + [_I] * 7 + [ctypes.c_double, _I, _I, _P, _P,
                                                                  ctypes.POINTER(_I)],
     "qtt_amen_solve": [_VP, _VP, _VP, _VP, ctypes.c_void_p, _P, ctypes.c_int64, ctypes.POINTER(_VP),
                        ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), _P],
@@ -88,7 +90,7 @@ class AmenParams(ctypes.Structure):
         ("enrichment_rank", ctypes.c_int), ("local_iterative", ctypes.c_int),
         ("direct_dim_cap", ctypes.c_int), ("local_iter_cap", ctypes.c_int),
         ("round_tol", ctypes.c_double), ("round_max_rank", ctypes.c_int),
-        ("stagnation_strikes", ctypes.c_int),
+        ("stagnation_strikes", ctypes.c_int), ("fused_cg", ctypes.c_int),
     ]
 
 
@@ -99,7 +101,7 @@ class AmenReport(ctypes.Structure):
         ("certifications_gram", ctypes.c_int), ("certifications_exact", ctypes.c_int),
         ("draws_used", ctypes.c_int64),
     ]
-_RESTYPES = {"qtt_last_error": ctypes.c_char_p, "qtt_ctx_stream": _VP}
+_RESTYPES = {"qtt_last_error": ctypes.c_char_p, "qtt_ctx_stream": _VP, "qtt_launch_count": ctypes.c_int64}
 
 
 def load_library(path: str = LIB_PATH):
@@ -169,8 +171,12 @@ class Context:
     def stream(self) -> int:
         return _lib.qtt_ctx_stream(self.handle)
 
-    def set_profiling(self, on: bool):
-        call("qtt_ctx_set_profiling", self.handle, 1 if on else 0)
+    def set_profiling(self, on, phases: bool = False):
+        """on: CUDA-event timing of K1/K2 launches; phases: synchronizing per-phase wall timing."""
+        call("qtt_ctx_set_profiling", self.handle, (1 if on else 0) | (2 if phases else 0))
+
+    def flush_l2(self):
+        call("qtt_ctx_flush_l2", self.handle)
 
     def stats(self) -> dict:
         s = QttStats()
@@ -203,6 +209,10 @@ def default_context(device: int = 0) -> Context:
         ctx = Context(device)
         _default_ctx[device] = ctx
     return ctx
+
+
+def launch_count() -> int:
+    return int(load_library().qtt_launch_count())
 
 
 def dptr(a: np.ndarray):

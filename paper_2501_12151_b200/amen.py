@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 import time
 from dataclasses import dataclass
 
@@ -41,6 +42,10 @@ __all__ = ["AmenConfig", "SolveReport", "amen_solve", "residual_norm"]
 
 DIRECT = "direct"
 ITERATIVE = "iterative"
+
+# Local CG engine: 1 = one persistent cooperative kernel per local solve (default),
+# 0 = per-step kernel launches (kept for A/B measurements).
+FUSED_CG = int(os.environ.get("QTT_FUSED_CG", "1"))
 
 # reference private helpers, same names (amen.py:108-160)
 _phi_left_step = _k.phi_left_step
@@ -149,6 +154,7 @@ def _params(config: AmenConfig) -> nat.AmenParams:
     p.round_tol = config.rounding.rel_tolerance
     p.round_max_rank = 0 if config.rounding.max_rank is None else config.rounding.max_rank
     p.stagnation_strikes = config.stagnation_strikes
+    p.fused_cg = FUSED_CG
     return p
 
 

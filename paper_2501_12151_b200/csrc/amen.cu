@@ -4,9 +4,14 @@
 // (polled in chunks), the per-sweep estimate and the certification.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "amen.cuh"
+#include "cg_fused.cuh"
+#include "chol_fused.cuh"
 #include "contract.cuh"
 #include "gemm.cuh"
 #include "linalg.cuh"
@@ -252,10 +257,18 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     DBuf sc(local_dense_scratch(L.lb, L.lo, L.lk, L.m, L.n, L.R1), c_.stream);
     local_dense(L.phil, L.lb, L.lo, L.lk, L.A, L.m, L.n, L.R1, L.phir, L.rb, L.rk, M.p, {sc.p, sc.n},
                 c_.stream);
-    max_abs_row_sum(c_, M.p, (int)dim, dim, c_.scal + 8);
-    potrf_lower(c_, M.p, (int)dim, dim, c_.flags + 3);
     QTT_CUDA(cudaMemcpyAsync(u.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
-    potrs_lower(c_, M.p, (int)dim, dim, u.p);
+    if (prm_.fused_cg) {  // one cooperative kernel: row sums + Cholesky + both solves
+      QTT_CUDA(cudaMemsetAsync(c_.scal + 8, 0, 8, c_.stream));
+      QTT_CUDA(cudaMemsetAsync(c_.flags + 3, 0, 4, c_.stream));
+      CholArgs ca{M.p, (int)dim, dim, u.p, c_.scal + 8, c_.flags + 3};
+      chol_fused_launch(ca, chol_fused_grid(c_.device), c_.stream);
+      c_.stats.chol_solves++;
+    } else {
+      max_abs_row_sum(c_, M.p, (int)dim, dim, c_.scal + 8);
+      potrf_lower(c_, M.p, (int)dim, dim, c_.flags + 3);
+      potrs_lower(c_, M.p, (int)dim, dim, u.p);
+    }
     double* pin = c_.host_scalars(2);
     QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 8, 8, cudaMemcpyDeviceToHost, c_.stream));
     QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 3, 4, cudaMemcpyDeviceToHost, c_.stream));
@@ -299,6 +312,44 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
   QTT_CUDA(cudaMemcpyAsync(u.p, prev_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
   QTT_CUDA(cudaMemcpyAsync(r.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
   const double kflops = local_matvec_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk);
+  if (prm_.fused_cg) {
+    // one persistent cooperative kernel for the whole CG solve (cg_fused.cu)
+    const int grid = cg_fused_grid(c_.device);
+    int S3 = 1, ktp = 1;
+    cg_fused_plan(L.lb, L.m, L.rb, L.R1, L.rk, grid, S3, ktp);
+    DBuf t1((long long)L.lb * L.lo * L.n * L.rk, c_.stream), t2((long long)L.lb * L.m * L.R1 * L.rk, c_.stream);
+    DBuf part3((long long)S3 * dim, c_.stream), red(2LL * grid, c_.stream);
+    CGFusedArgs a{};
+    a.phil = L.phil; a.lb = L.lb; a.lo = L.lo; a.lk = L.lk;
+    a.Ap = L.Ap; a.m = L.m; a.n = L.n; a.R1 = L.R1;
+    a.phir = L.phir; a.rb = L.rb; a.rk = L.rk;
+    a.b = rhs_p; a.invd = invd.p; a.x = u.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
+    a.t1 = t1.p; a.t2 = t2.p; a.part3 = part3.p; a.S3 = S3; a.kt_per3 = ktp; a.red = red.p;
+    a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;
+    a.out_iters = c_.flags + 8;
+    a.out_rnorm = c_.scal + 20;
+    a.out_mv_ns = (unsigned long long*)(c_.scal + 21);
+    QTT_CUDA(cudaMemsetAsync(c_.scal + 21, 0, 8, c_.stream));
+    cg_fused_launch(a, grid, c_.stream);
+    double* pin = c_.host_scalars(2);
+    QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 21, 8, cudaMemcpyDeviceToHost, c_.stream));
+    QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 8, 4, cudaMemcpyDeviceToHost, c_.stream));
+    c_.sync();
+    unsigned long long ns;
+    std::memcpy(&ns, pin, 8);
+    int it;
+    std::memcpy(&it, pin + 1, 4);
+    iters = it;
+    const int calls = it + (xany ? 1 : 0);
+    c_.stats.cg_iters += it;
+    c_.stats.k1_calls += calls;
+    c_.stats.k1_flops += kflops * calls;
+    if (c_.profiling) {
+      c_.stats.k1_ms += ns * 1e-6;
+      c_.stats.k1_timed_flops += kflops * calls;
+    }
+    return u;
+  }
   int* flags = c_.flags;
   if (xany) {  // r = b - A x0
     const int t = c_.prof_begin();
@@ -815,7 +866,13 @@ Train Solver::run(const Train* x0, AmenResult& res) {
     }
     bool gram = false;
     c_.phase(PH_CERT);
+    const auto tc0 = std::chrono::steady_clock::now();
     final_res = residual_norm(c_, A_, xcur, f_, &gram);
+    if (std::getenv("QTT_DEBUG"))
+      std::fprintf(stderr, "[qtt] sweep %d certification %.6g (%s) %.3f s, max rank %d\n", sw, final_res,
+                   gram ? "gram" : "exact",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count(),
+                   *std::max_element(rk.begin(), rk.end()));
     c_.phase(PH_OTHER);
     (gram ? res.certifications_gram : res.certifications_exact)++;
     have_final = true;

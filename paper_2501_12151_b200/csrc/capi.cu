@@ -32,6 +32,7 @@ Ctx::Ctx(int dev) : device(dev) {
 }
 
 Ctx::~Ctx() {
+  l2_flush.release();
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
@@ -49,7 +50,7 @@ long long launch_count() { return g_launches.load(); }
 void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void Ctx::phase(int ph) {
-  if (!profiling) return;
+  if (!phase_sync) return;
   sync();
   const double t = std::chrono::duration<double, std::milli>(
                        std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -167,9 +168,22 @@ void* qtt_ctx_stream(qtt_ctx* ctx) { return ctx ? (void*)ctx->impl.stream : null
 int qtt_ctx_set_profiling(qtt_ctx* ctx, int on) {
   return guarded([&] {
     check_ctx(ctx);
-    ctx->impl.profiling = on != 0;
+    ctx->impl.profiling = (on & 1) != 0;
+    ctx->impl.phase_sync = (on & 2) != 0;
   });
 }
+
+int qtt_ctx_flush_l2(qtt_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    qtt::Ctx& c = ctx->impl;
+    const long long n = 256LL << 20;  // 256 MiB > 126 MB L2
+    if (c.l2_flush.n < n / 8) c.l2_flush.alloc(n / 8, c.stream);
+    QTT_CUDA(cudaMemsetAsync(c.l2_flush.p, 0, n, c.stream));
+  });
+}
+
+int64_t qtt_launch_count(void) { return qtt::launch_count(); }
 
 int qtt_ctx_get_stats(qtt_ctx* ctx, qtt_stats* o) {
   return guarded([&] {

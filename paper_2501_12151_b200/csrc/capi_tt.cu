@@ -252,6 +252,7 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
     p.round_tol = prm->round_tol;
     p.round_max_rank = prm->round_max_rank;
     p.stagnation_strikes = prm->stagnation_strikes;
+    p.fused_cg = prm->fused_cg;
     qtt::DrawStream ds;
     ds.p = draws;
     ds.n = n_draws;
@@ -277,8 +278,8 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
 
 int qtt_local_solve(qtt_ctx* ctx, const double* phil, const double* A, const double* phir,
                     const double* rhs, const double* prev, int rl, int R0, int m, int R1, int rr,
-                    int iterative, int direct_dim_cap, double residual_tol, int iter_cap, double* u,
-                    double* lam, int* iterations) {
+                    int iterative, int direct_dim_cap, double residual_tol, int iter_cap, int fused_cg,
+                    double* u, double* lam, int* iterations) {
   return guarded([&] {
     qtt::Ctx& c = C(ctx);
     if (rl < 1 || R0 < 1 || m < 1 || R1 < 1 || rr < 1) throw qtt::Error(QTT_ERR_SHAPE, "bad local shape");
@@ -297,6 +298,7 @@ int qtt_local_solve(qtt_ctx* ctx, const double* phil, const double* A, const dou
     p.direct_dim_cap = direct_dim_cap;
     p.residual_tol = residual_tol;
     p.local_iter_cap = iter_cap;
+    p.fused_cg = fused_cg;
     double l = 0;
     int it = 0;
     qtt::DBuf du = qtt::solve_local_system(c, L, db.p, dp.p, p, 0, 0, l, it, false);

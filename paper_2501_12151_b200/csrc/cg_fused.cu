@@ -1,0 +1,235 @@
+// Persistent, cooperative Jacobi-PCG for one AMEn local system (amen.py:192-214):
+// every iteration -- the three-GEMM local matvec (amen.py:134-137) on the DMMA tile
+// engine, the split-K reduction, the dot products and the vector updates -- runs
+// inside ONE kernel launch, phases separated by grid-wide barriers, so nothing
+// leaves HBM/L2 between iterations and there is no per-iteration launch or host
+// round trip (north_star item c).  Reductions are fixed-order (deterministic) and
+// every CTA evaluates the same scalar recurrence, so all CTAs agree on the SciPy
+// stopping rule  ||r|| < rtol*||b||  checked before each step.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "cg_fused.cuh"
+#include "dmma_tile.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace qtt {
+namespace {
+
+using CF = tile::Cfg<64, 64, 16, 2, 4, 3>;  // 256 threads, warp tile 32x16
+constexpr int NT = CF::NT;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sums of two values, broadcast (red: >= 20 doubles of shared memory)
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) { red[warp] = a; red[8 + warp] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < NT / 32 ? red[lane] : 0.0, y = lane < NT / 32 ? red[8 + lane] : 0.0;
+    x = warp_sum(x);
+    y = warp_sum(y);
+    if (lane == 0) { red[16] = x; red[17] = y; }
+  }
+  __syncthreads();
+  a = red[16];
+  b = red[17];
+  __syncthreads();
+}
+
+// Sum the per-CTA partials part[2*i + {0,1}] in a fixed order (identical in every CTA).
+__device__ __forceinline__ void grid_sum2(const double* part, int nparts, double& a, double& b, double* red) {
+  a = 0.0;
+  b = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += NT) {
+    a += __ldcg(part + 2 * i);
+    b += __ldcg(part + 2 * i + 1);
+  }
+  block_sum2(a, b, red);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One GEMM phase: every CTA takes work items blockIdx.x, +gridDim.x, ...
+// C[b][r*c_rs + c] = sum_k op(A_b)(r,k) op(B_b)(k,c)   (split-K when splits > 1:
+// item writes its partial into C + s*split_stride instead)
+__device__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b_bs, int batch, double* C,
+                           long long c_rs, long long c_bs, int splits, int kt_per, long long split_stride,
+                           double* smem) {
+  const int tm = (o0.M + CF::BM - 1) / CF::BM, tn = (o0.N + CF::BN - 1) / CF::BN;
+  const int ktiles = (o0.K + CF::BK - 1) / CF::BK;
+  const long long per_batch = (long long)tm * tn * splits;
+  const long long items = per_batch * batch;
+  for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int b = (int)(it / per_batch);
+    long long rem = it % per_batch;
+    const int s = (int)(rem % splits);
+    rem /= splits;
+    const int ti = (int)(rem / tn), tj = (int)(rem % tn);
+    tile::Operands o = o0;
+    o.A += b * a_bs;
+    o.B += b * b_bs;
+    double acc[CF::MI][CF::NI][2];
+    tile::zero_acc<CF>(acc);
+    const int k0 = s * kt_per, k1 = min(ktiles, k0 + kt_per);
+    tile::mma_tile<CF>(o, ti * CF::BM, tj * CF::BN, k0, k1, smem, acc);
+    double* Cb = C + b * c_bs + s * split_stride;
+    tile::for_each_acc<CF>(ti * CF::BM, tj * CF::BN, o.M, o.N, acc,
+                           [&](int r, int c, double v) { Cb[(long long)r * c_rs + c] = v; });
+  }
+}
+
+// q = A v  for the local operator, leaves q = sum of the split-K partials of step 3
+// unreduced in a.part3; returns after a grid barrier.
+__device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* smem, cg::grid_group& grid) {
+  // step 1: t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
+  tile::Operands o1{a.phil, a.lk, 1, v, (long long)a.n * a.rk, 1, a.lb * a.lo, a.n * a.rk, a.lk};
+  phase_gemm(o1, 0, 0, 1, a.t1, (long long)a.n * a.rk, 0, 1, (o1.K + CF::BK - 1) / CF::BK, 0, smem);
+  grid.sync();
+  // step 2: per X: t2[X][(m,b),V] = Ap[(m,b),(a,n)] @ t1[X][(a,n),V]
+  tile::Operands o2{a.Ap, (long long)a.lo * a.n, 1, a.t1, a.rk, 1, a.m * a.R1, a.rk, a.lo * a.n};
+  phase_gemm(o2, 0, (long long)a.lo * a.n * a.rk, a.lb, a.t2, a.rk, (long long)a.m * a.R1 * a.rk, 1,
+             (o2.K + CF::BK - 1) / CF::BK, 0, smem);
+  grid.sync();
+  // step 3 (split-K): part3[s][(X,m),Y] = t2[(X,m),(b,V)] @ phir[Y,(b,V)]^T
+  tile::Operands o3{a.t2, (long long)a.R1 * a.rk, 1, a.phir, 1, (long long)a.R1 * a.rk, a.lb * a.m, a.rb,
+                    a.R1 * a.rk};
+  phase_gemm(o3, 0, 0, 1, a.part3, a.rb, 0, a.S3, a.kt_per3, (long long)a.lb * a.m * a.rb, smem);
+  grid.sync();
+}
+
+__device__ __forceinline__ double reduce_q(const CGFusedArgs& a, long long e) {
+  double s = 0.0;
+  const long long stride = a.dim;
+  for (int k = 0; k < a.S3; ++k) s += __ldcg(a.part3 + k * stride + e);
+  return s;
+}
+
+__global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
+  extern __shared__ double smem[];
+  __shared__ double red[24];
+  cg::grid_group grid = cg::this_grid();
+  const long long n = a.dim;
+  // contiguous slice of the vectors owned by this CTA
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long e0 = blockIdx.x * per, e1 = min(n, e0 + per);
+  unsigned long long mv_ns = 0, t0;
+  const bool timer = (blockIdx.x == 0 && threadIdx.x == 0);
+
+  // ---- r = b - A x0 (only when x0 has a nonzero entry, as scipy's `x.any()`)
+  if (a.xany) {
+    if (timer) t0 = gtimer();
+    matvec_phases(a, a.x, smem, grid);
+    if (timer) mv_ns += gtimer() - t0;
+  }
+  double rr = 0.0, rz = 0.0;
+  for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
+    const double ri = a.xany ? __ldcg(a.b + e) - reduce_q(a, e) : __ldcg(a.b + e);
+    const double zi = ri * a.invd[e];
+    a.r[e] = ri;
+    a.z[e] = zi;
+    a.p[e] = zi;
+    rr += ri * ri;
+    rz += ri * zi;
+  }
+  block_sum2(rr, rz, red);
+  if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = rr; a.red[2 * blockIdx.x + 1] = rz; }
+  grid.sync();
+  grid_sum2(a.red, gridDim.x, rr, rz, red);
+  double rho = rz, rnorm = sqrt(rr);
+  int it = 0;
+  grid.sync();  // everyone has read red[] before it is reused
+
+  while (!(rnorm < a.atol) && it < a.maxiter) {
+    // ---- q = A p
+    if (timer) t0 = gtimer();
+    matvec_phases(a, a.p, smem, grid);
+    // ---- reduce q, p.q
+    double pq = 0.0, dummy = 0.0;
+    for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
+      const double qi = reduce_q(a, e);
+      a.q[e] = qi;
+      pq += __ldcg(a.p + e) * qi;
+    }
+    block_sum2(pq, dummy, red);
+    if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = pq; a.red[2 * blockIdx.x + 1] = 0.0; }
+    grid.sync();
+    if (timer) mv_ns += gtimer() - t0;
+    grid_sum2(a.red, gridDim.x, pq, dummy, red);
+    const double alpha = rho / pq;
+    grid.sync();
+    // ---- x += alpha p; r -= alpha q; z = M^-1 r; rr, rz
+    rr = 0.0;
+    rz = 0.0;
+    for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
+      const double pi = __ldcg(a.p + e);
+      a.x[e] += alpha * pi;
+      const double ri = a.r[e] - alpha * a.q[e];
+      a.r[e] = ri;
+      const double zi = ri * a.invd[e];
+      a.z[e] = zi;
+      rr += ri * ri;
+      rz += ri * zi;
+    }
+    block_sum2(rr, rz, red);
+    if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = rr; a.red[2 * blockIdx.x + 1] = rz; }
+    grid.sync();
+    grid_sum2(a.red, gridDim.x, rr, rz, red);
+    ++it;
+    rnorm = sqrt(rr);
+    if (rnorm < a.atol || it >= a.maxiter) break;
+    const double beta = rz / rho;
+    rho = rz;
+    for (long long e = e0 + threadIdx.x; e < e1; e += NT) a.p[e] = a.z[e] + beta * a.p[e];
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.out_iters = it;
+    *a.out_rnorm = rnorm;
+    *a.out_mv_ns += mv_ns;
+  }
+}
+
+}  // namespace
+
+int cg_fused_grid(int device) {
+  static int cached = -1;
+  if (cached > 0) return cached;
+  QTT_CUDA(cudaFuncSetAttribute(cg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+  int per_sm = 0, sms = 0;
+  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, NT, CF::SMEM));
+  QTT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  cached = std::max(1, std::min(per_sm, 2)) * sms;
+  return cached;
+}
+
+void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3) {
+  const int M3 = lb * m, N3 = rb, K3 = R1 * rk;
+  const int tiles = cdiv(M3, CF::BM) * cdiv(N3, CF::BN);
+  const int ktiles = cdiv(K3, CF::BK);
+  int want = std::max(1, std::min(cdiv(grid, tiles), std::max(1, ktiles / 4)));
+  kt_per3 = cdiv(ktiles, want);
+  S3 = cdiv(ktiles, kt_per3);
+}
+
+void cg_fused_launch(const CGFusedArgs& a, int grid, cudaStream_t s) {
+  void* args[] = {(void*)&a};
+  QTT_CUDA(cudaLaunchCooperativeKernel((void*)cg_fused_kernel, dim3(grid), dim3(NT), args, CF::SMEM, s));
+  QTT_CHECK_LAUNCH();
+}
+
+}  // namespace qtt

@@ -1,0 +1,40 @@
+// Persistent cooperative Jacobi-PCG for one local system (see cg_fused.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qtt {
+
+struct CGFusedArgs {
+  // local operator: phil (lb, lo, lk), Ap = permuted core (m, R1 | lo, n), phir (rb, R1, rk)
+  const double* phil;
+  int lb, lo, lk;
+  const double* Ap;
+  int m, n, R1;
+  const double* phir;
+  int rb, rk;
+  // vectors of length dim = lb*m*rb (== lk*n*rk for the symmetric local operator)
+  const double* b;
+  const double* invd;
+  double* x;  // in: x0, out: solution
+  double *r, *z, *p, *q;
+  // scratch
+  double* t1;     // lb*lo*n*rk
+  double* t2;     // lb*m*R1*rk
+  double* part3;  // S3*dim split-K partials of step 3
+  int S3, kt_per3;
+  double* red;  // 2*grid doubles
+  long long dim;
+  double atol;
+  int maxiter;
+  int xany;
+  // outputs (device)
+  int* out_iters;
+  double* out_rnorm;
+  unsigned long long* out_mv_ns;  // accumulated wall ns spent in the local matvecs
+};
+
+int cg_fused_grid(int device);
+void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3);
+void cg_fused_launch(const CGFusedArgs& a, int grid, cudaStream_t s);
+
+}  // namespace qtt

@@ -52,51 +52,6 @@ struct TraceRec {
   int sweep, core, rl, m, rr, zl, zr, R0, R1, path /*0 direct, 1 cg*/, iters;
 };
 
-struct Ctx {
-  int device = 0;
-  std::vector<TraceRec> trace;
-  cudaStream_t stream = nullptr;
-  bool profiling = false;
-  Stats stats;
-  // pinned host staging for small scalar readbacks
-  double* pinned = nullptr;
-  size_t pinned_n = 0;
-  std::vector<cudaEvent_t> ev_pool;
-  // deterministic-reduction scratch (linalg.cu) and small device flags
-  double* red_partial = nullptr;   // 1024 doubles
-  unsigned* red_counter = nullptr; // 1 counter
-  int* flags = nullptr;            // 64 ints (Cholesky info, CG done, ...)
-  double* scal = nullptr;          // 256 device scalars
-  Profiler prof;
-  explicit Ctx(int dev);
-  ~Ctx();
-  // profiling helpers (no-ops unless profiling): begin returns a record id or -1
-  int prof_begin() {
-    if (!profiling) return -1;
-    Profiler::Rec r{prof.get(), prof.get(), 0, 0.0, true};
-    QTT_CUDA(cudaEventRecord(r.a, stream));
-    prof.pending.push_back(r);
-    return (int)prof.pending.size() - 1;
-  }
-  void prof_end(int id, int kind, double flops) {
-    if (id < 0) return;
-    auto& r = prof.pending[id];
-    QTT_CUDA(cudaEventRecord(r.b, stream));
-    r.kind = kind;
-    r.flops = flops;
-  }
-  void prof_discard(int id) {
-    if (id >= 0) prof.pending[id].keep = false;
-  }
-  // resolve pending records (synchronizes the stream)
-  void prof_flush();
-  int phase_cur = 0;
-  double phase_t0 = -1;
-  void phase(int ph);
-  double* host_scalars(size_t n);
-  void sync() { QTT_CUDA(cudaStreamSynchronize(stream)); }
-};
-
 // Stream-ordered device buffer (cudaMallocAsync on the context stream).
 struct DBuf {
   double* p = nullptr;
@@ -130,5 +85,54 @@ struct DBuf {
     QTT_CUDA(cudaMemcpyAsync(h, p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, s));
   }
 };
+
+struct Ctx {
+  int device = 0;
+  std::vector<TraceRec> trace;
+  cudaStream_t stream = nullptr;
+  bool profiling = false;   // CUDA-event timing of K1/K2 launches (deferred, no syncs)
+  bool phase_sync = false;  // per-phase wall timing (synchronizes at phase boundaries)
+  Stats stats;
+  // pinned host staging for small scalar readbacks
+  double* pinned = nullptr;
+  size_t pinned_n = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  // deterministic-reduction scratch (linalg.cu) and small device flags
+  double* red_partial = nullptr;   // 1024 doubles
+  unsigned* red_counter = nullptr; // 1 counter
+  int* flags = nullptr;            // 64 ints (Cholesky info, CG done, ...)
+  double* scal = nullptr;          // 256 device scalars
+  Profiler prof;
+  DBuf l2_flush;  // scratch written between timed steps (bench L2 flush)
+  explicit Ctx(int dev);
+  ~Ctx();
+  // profiling helpers (no-ops unless profiling): begin returns a record id or -1
+  int prof_begin() {
+    if (!profiling) return -1;
+    Profiler::Rec r{prof.get(), prof.get(), 0, 0.0, true};
+    QTT_CUDA(cudaEventRecord(r.a, stream));
+    prof.pending.push_back(r);
+    return (int)prof.pending.size() - 1;
+  }
+  void prof_end(int id, int kind, double flops) {
+    if (id < 0) return;
+    auto& r = prof.pending[id];
+    QTT_CUDA(cudaEventRecord(r.b, stream));
+    r.kind = kind;
+    r.flops = flops;
+  }
+  void prof_discard(int id) {
+    if (id >= 0) prof.pending[id].keep = false;
+  }
+  // resolve pending records (synchronizes the stream)
+  void prof_flush();
+  int phase_cur = 0;
+  double phase_t0 = -1;
+  void phase(int ph);
+  double* host_scalars(size_t n);
+  void sync() { QTT_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+
 
 }  // namespace qtt

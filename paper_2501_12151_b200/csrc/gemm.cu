@@ -1,179 +1,49 @@
-// FP64 DMMA GEMM (see gemm.cuh for the operand convention).
-#include "gemm.cuh"
-
+// FP64 DMMA GEMM (see gemm.cuh for the operand convention); the tile engine
+// itself lives in dmma_tile.cuh and is shared with the persistent fused kernels.
 #include <algorithm>
+
+#include "dmma_tile.cuh"
+#include "gemm.cuh"
 
 namespace qtt {
 namespace {
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
-struct Cfg {
-  static constexpr int NT = WARPS_M * WARPS_N * 32;
-  static constexpr int LDA = BM + 4;  // == 4 (mod 16) doubles: conflict-free fragment loads
-  static constexpr int LDB = BN + 4;
-  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
-  static constexpr int MI = WTM / 8, NI = WTN / 8;
-  static constexpr size_t SMEM = (size_t)STAGES * BK * (LDA + LDB) * sizeof(double);
-  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8");
-  static_assert((BM * BK) % NT == 0 && (BN * BK) % NT == 0, "tile loads must divide evenly");
-  static_assert(BK % 4 == 0 && BM % 4 == 0 && BN % 4 == 0, "4x4 swizzle");
-};
-
-// Element index e of a (BK x BX) tile -> (kk, xx).  When the global operand is
-// contiguous along X, consecutive threads walk X (coalesced, conflict-free STS).
-// Otherwise (contiguous along K) a 4x4 micro-block swizzle keeps 32-byte global
-// sectors and spreads the 16 lanes of a half-warp over 16 distinct banks.
-template <int BK>
-__device__ __forceinline__ void tile_coord(int e, bool x_contig, int BX, int& kk, int& xx) {
-  if (x_contig) {
-    xx = e % BX;
-    kk = e / BX;
-  } else {
-    int kq = e & 3, xq = (e >> 2) & 3, blk = e >> 4;
-    kk = (blk % (BK / 4)) * 4 + kq;
-    xx = (blk / (BK / 4)) * 4 + xq;
-  }
-}
-
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
+template <class C>
+__global__ void __launch_bounds__(C::NT)
     dgemm_kernel(GemmArgs g, int splits, int kt_per_split, double* __restrict__ ws) {
-  using C_ = Cfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
-  constexpr int NT = C_::NT, LDA = C_::LDA, LDB = C_::LDB, MI = C_::MI, NI = C_::NI;
   extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + STAGES * BK * LDA;
-
   if (g.skip != nullptr && *g.skip != 0) return;
-  if (g.lower_only && (int)(blockIdx.x * BN) >= (int)(blockIdx.y * BM + BM)) return;
+  if (g.lower_only && (int)(blockIdx.x * C::BN) >= (int)(blockIdx.y * C::BM + C::BM)) return;
   int z = blockIdx.z;
   const int split = z % splits;
   z /= splits;
   const int b1 = z % g.batch1;
   const int b2 = z / g.batch1;
-  const double* __restrict__ A = g.A + b1 * g.a_bs1 + b2 * g.a_bs2;
-  const double* __restrict__ B = g.B + b1 * g.b_bs1 + b2 * g.b_bs2;
-  const int M = g.M, N = g.N, K = g.K;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int ktiles = (K + BK - 1) / BK;
+  tile::Operands o{g.A + b1 * g.a_bs1 + b2 * g.a_bs2, g.a_rs, g.a_cs,
+                   g.B + b1 * g.b_bs1 + b2 * g.b_bs2, g.b_rs, g.b_cs, g.M, g.N, g.K};
+  const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * C::BN;
+  const int ktiles = (g.K + C::BK - 1) / C::BK;
   const int kt_begin = split * kt_per_split;
   const int kt_end = min(ktiles, kt_begin + kt_per_split);
-  const bool a_mc = (g.a_rs == 1);
-  const bool b_nc = (g.b_cs == 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm0 = (warp % WARPS_M) * C_::WTM;
-  const int wn0 = (warp / WARPS_M) * C_::WTN;
-  const int lr = lane >> 2, lc = lane & 3;
-
-  double acc[MI][NI][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  auto load_tile = [&](int kt, int stage) {
-    const int k0 = kt * BK;
-    double* dA = sA + stage * BK * LDA;
-    double* dB = sB + stage * BK * LDB;
-#pragma unroll
-    for (int i = 0; i < (BM * BK) / NT; ++i) {
-      int kk, mm;
-      tile_coord<BK>(threadIdx.x + i * NT, a_mc, BM, kk, mm);
-      const int gm = m0 + mm, gk = k0 + kk;
-      const bool ok = gm < M && gk < K;
-      const double* src = ok ? A + (long long)gm * g.a_rs + (long long)gk * g.a_cs : A;
-      cp_async8(dA + kk * LDA + mm, src, ok);
-    }
-#pragma unroll
-    for (int i = 0; i < (BN * BK) / NT; ++i) {
-      int kk, nn;
-      tile_coord<BK>(threadIdx.x + i * NT, b_nc, BN, kk, nn);
-      const int gn = n0 + nn, gk = k0 + kk;
-      const bool ok = gn < N && gk < K;
-      const double* src = ok ? B + (long long)gk * g.b_rs + (long long)gn * g.b_cs : B;
-      cp_async8(dB + kk * LDB + nn, src, ok);
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (kt_begin + s < kt_end) load_tile(kt_begin + s, s);
-    cp_async_commit();
-  }
-
-  for (int kt = kt_begin; kt < kt_end; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int stage = (kt - kt_begin) % STAGES;
-    const int nk = kt + STAGES - 1;
-    if (nk < kt_end) load_tile(nk, (nk - kt_begin) % STAGES);
-    cp_async_commit();
-
-    const double* cA = sA + stage * BK * LDA;
-    const double* cB = sB + stage * BK * LDB;
-#pragma unroll
-    for (int ks = 0; ks < BK; ks += 4) {
-      double af[MI], bf[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) af[i] = cA[(ks + lc) * LDA + wm0 + i * 8 + lr];
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[j] = cB[(ks + lc) * LDB + wn0 + j * 8 + lr];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma(acc[i][j], af[i], bf[j]);
-    }
-  }
-  cp_async_wait<0>();
-
+  double acc[C::MI][C::NI][2];
+  tile::zero_acc<C>(acc);
+  tile::mma_tile<C>(o, m0, n0, kt_begin, kt_end, smem, acc);
   if (splits > 1) {
-    double* W = ws + (long long)split * M * N;
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int row = m0 + wm0 + i * 8 + lr;
-        const int col = n0 + wn0 + j * 8 + lc * 2;
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-          if (row < M && col + t < N) W[(long long)row * N + col + t] = acc[i][j][t];
-      }
+    double* W = ws + (long long)split * g.M * g.N;
+    const int N = g.N;
+    tile::for_each_acc<C>(m0, n0, g.M, g.N, acc, [&](int r, int c, double v) { W[(long long)r * N + c] = v; });
     return;
   }
-  double* C = g.C + b1 * g.c_bs1 + b2 * g.c_bs2;
+  double* Cp = g.C + b1 * g.c_bs1 + b2 * g.c_bs2;
   const double alpha = g.alpha, beta = g.beta;
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-      const int row = m0 + wm0 + i * 8 + lr;
-      const int col = n0 + wn0 + j * 8 + lc * 2;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (row < M && col + t < N && (!g.lower_only || col + t <= row)) {
-          double* p = C + (long long)row * g.c_rs + (long long)(col + t) * g.c_cs;
-          double v = alpha * acc[i][j][t];
-          if (beta != 0.0) v = fma(beta, *p, v);
-          *p = v;
-        }
-      }
-    }
+  const bool lower = g.lower_only;
+  tile::for_each_acc<C>(m0, n0, g.M, g.N, acc, [&](int r, int c, double v) {
+    if (lower && c > r) return;
+    double* p = Cp + (long long)r * g.c_rs + (long long)c * g.c_cs;
+    double out = alpha * v;
+    if (beta != 0.0) out = fma(beta, *p, out);
+    *p = out;
+  });
 }
 
 __global__ void splitk_reduce(const double* __restrict__ ws, int splits, int M, int N, double* C,
@@ -193,21 +63,24 @@ __global__ void splitk_reduce(const double* __restrict__ ws, int splits, int M, 
   }
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST>
+template <class C>
 void launch(const GemmArgs& g, int splits, int kt_per, double* ws, cudaStream_t s) {
-  using C_ = Cfg<BM, BN, BK, WM, WN, ST>;
   static bool attr_set = false;  // per-instantiation, set once per process
   if (!attr_set) {
-    QTT_CUDA(cudaFuncSetAttribute(dgemm_kernel<BM, BN, BK, WM, WN, ST>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM));
+    QTT_CUDA(cudaFuncSetAttribute(dgemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM));
     attr_set = true;
   }
   long long zb = (long long)g.batch1 * g.batch2 * splits;
   if (zb > 65535) throw Error(QTT_ERR_ARG, "gemm: batch too large for grid.z");
-  dim3 grid(cdiv(g.N, BN), cdiv(g.M, BM), (unsigned)zb);
-  dgemm_kernel<BM, BN, BK, WM, WN, ST><<<grid, C_::NT, C_::SMEM, s>>>(g, splits, kt_per, ws);
+  dim3 grid(cdiv(g.N, C::BN), cdiv(g.M, C::BM), (unsigned)zb);
+  dgemm_kernel<C><<<grid, C::NT, C::SMEM, s>>>(g, splits, kt_per, ws);
   QTT_CHECK_LAUNCH();
 }
+
+using Cfg64 = tile::Cfg<64, 64, 16, 2, 2, 3>;
+using Cfg32 = tile::Cfg<32, 32, 16, 2, 2, 4>;
+using Cfg128 = tile::Cfg<128, 64, 16, 4, 2, 3>;
 
 constexpr int kSMs = 148;
 
@@ -269,9 +142,9 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
     p.kt_per = cdiv(g.K, 16);
   }
   switch (p.cfg) {
-    case 1: launch<32, 32, 16, 2, 2, 4>(g, p.splits, p.kt_per, ws, s); break;
-    case 2: launch<128, 64, 16, 4, 2, 3>(g, p.splits, p.kt_per, ws, s); break;
-    default: launch<64, 64, 16, 2, 2, 3>(g, p.splits, p.kt_per, ws, s); break;
+    case 1: launch<Cfg32>(g, p.splits, p.kt_per, ws, s); break;
+    case 2: launch<Cfg128>(g, p.splits, p.kt_per, ws, s); break;
+    default: launch<Cfg64>(g, p.splits, p.kt_per, ws, s); break;
   }
   if (p.splits > 1) {
     const long long total = (long long)g.M * g.N;

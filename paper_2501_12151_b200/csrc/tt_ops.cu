@@ -2,6 +2,8 @@
 // and the residual norm of amen.py:87-99.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "contract.cuh"
 #include "gemm.cuh"
@@ -394,6 +396,9 @@ double residual_norm(Ctx& c, const Train& A, const Train& x, const Train& f, boo
   const double ff = tt_dot(c, f, f);
   const double r2 = aa - 2.0 * fa + ff;
   const double scale = std::fabs(aa) + 2.0 * std::fabs(fa) + std::fabs(ff);
+  if (std::getenv("QTT_DEBUG"))
+    std::fprintf(stderr, "[qtt] residual_norm gram: aa=%.17g fa=%.17g ff=%.17g r2=%.6g nf=%.6g\n", aa, fa, ff,
+                 r2, nf);
   // Accept the Gram value only when it is far above its rounding-error floor
   // (relative error of r2 <= ~1e-3 even with a 100x error growth); otherwise
   // fall back to the exact QR-sweep norm of the explicit difference train.
@@ -403,6 +408,7 @@ double residual_norm(Ctx& c, const Train& A, const Train& x, const Train& f, boo
     return nf > 0 ? nr / nf : nr;
   }
   if (used_gram) *used_gram = false;
+  if (std::getenv("QTT_DEBUG")) std::fprintf(stderr, "[qtt] residual_norm: exact QR-sweep fallback\n");
   return residual_norm_exact(c, A, x, f);
 }
 

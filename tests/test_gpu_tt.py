@@ -133,11 +133,13 @@ def test_local_solve_vs_reference():
     _, m, _, R1 = A.shape
     rr = phir.shape[0]
     ctx = nat.default_context()
-    for iterative, tol, key in [(0, 1e-8, "direct"), (1, 1e-8, "iter_u_1e-08"), (1, 1e-4, "iter_u_0.0001")]:
+    cases = [(0, 1e-8, "direct", 1), (1, 1e-8, "iter_u_1e-08", 0), (1, 1e-4, "iter_u_0.0001", 0),
+             (1, 1e-8, "iter_u_1e-08", 1), (1, 1e-4, "iter_u_0.0001", 1)]
+    for iterative, tol, key, fused in cases:
         u = np.empty((rl, m, rr))
         lam, its = ctypes.c_double(), ctypes.c_int()
         nat.call("qtt_local_solve", ctx.handle, nat.dptr(phil), nat.dptr(A), nat.dptr(phir), nat.dptr(rhs),
-                 nat.dptr(prev), rl, R0, m, R1, rr, iterative, 4096, tol, 400, nat.dptr(u),
+                 nat.dptr(prev), rl, R0, m, R1, rr, iterative, 4096, tol, 400, fused, nat.dptr(u),
                  ctypes.byref(lam), ctypes.byref(its))
         if key == "direct":
             assert rel(u, d["direct_u"]) <= 1e-12
@@ -147,3 +149,39 @@ def test_local_solve_vs_reference():
             assert rel(u, d[key]) <= max(10 * 0.05 * tol, 1e-11)
             lam_ref = float(d[key.replace("_u_", "_lam_")])
             assert abs(lam.value - lam_ref) <= 1e-12 * abs(lam_ref)
+
+
+@pytest.mark.parametrize("rl,R,rr", [(12, 7, 9), (40, 20, 36), (68, 49, 68)])
+def test_fused_cg_matches_stepwise_cg(rl, R, rr):
+    """The persistent cooperative CG kernel runs the same recurrence as the
+    per-step path and the oracle's SciPy-cg restatement on an SPD local system."""
+    from paper_2501_12151_b200 import _native as nat
+    rng = np.random.default_rng(rl * 100 + rr)
+    m = 2
+    # SPD environments: Gram matrices per operator slice, SPD operator core
+    gl = rng.standard_normal((R, rl, rl))
+    phil = np.einsum("aij,akj->iak", gl, gl) / rl + np.eye(rl)[:, None, :]
+    gr = rng.standard_normal((R, rr, rr))
+    phir = np.einsum("aij,akj->iak", gr, gr) / rr + np.eye(rr)[:, None, :]
+    G = rng.standard_normal((R, m, m, R)) / R
+    A = np.einsum("amnb,apnb->ampb", G, G)  # symmetric PSD in (m, p) per (a, b)
+    A = nat.f64(A + 0.5 * np.einsum("ab,mn->amnb", np.eye(R), np.eye(m)))
+    phil, phir = nat.f64(phil), nat.f64(phir)
+    rhs = nat.f64(rng.standard_normal((rl, m, rr)))
+    prev = nat.f64(rng.standard_normal((rl, m, rr)) * 0.1)
+    ctx = nat.default_context()
+    outs = []
+    for fused in (0, 1):
+        u = np.empty((rl, m, rr))
+        lam, its = ctypes.c_double(), ctypes.c_int()
+        nat.call("qtt_local_solve", ctx.handle, nat.dptr(phil), nat.dptr(A), nat.dptr(phir), nat.dptr(rhs),
+                 nat.dptr(prev), rl, R, m, R, rr, 1, 4096, 1e-6, 400, fused, nat.dptr(u),
+                 ctypes.byref(lam), ctypes.byref(its))
+        outs.append((u.copy(), its.value, lam.value))
+    (u0, i0, l0), (u1, i1, l1) = outs
+    assert abs(i0 - i1) <= 1
+    assert rel(u1, u0) <= 1e-9
+    assert abs(l0 - l1) <= 1e-12 * abs(l0)
+    uo, lo, info = O.solve_local(phil, A, phir, rhs, prev, direct=False, direct_cap=4096, tol=1e-6,
+                                 iter_cap=400, sweep=1, k=0)
+    assert rel(u1, uo) <= 1e-8 and abs(info["iters"] - i1) <= 1

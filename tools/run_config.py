@@ -34,7 +34,7 @@ def main():
     cfg = AmenConfig(rounding=TruncationPolicy(rel, cap), **kw)
     A, f, X0 = TTLinearOperator(prob.op), TensorTrain(prob.rhs), TensorTrain(x0)
     ctx = nat.default_context()
-    ctx.set_profiling(a.profile)
+    ctx.set_profiling(a.profile, phases=a.profile)
     # warm-up on a tiny problem (module load, kernel attributes)
     ctx.reset_stats()
     t0 = time.perf_counter()
