@@ -128,10 +128,11 @@ int qtt_tt_round(qtt_ctx* ctx, const qtt_train* a, double rel_tol, int max_rank,
                  qtt_train** out);                                            /* tt.py:409, 506 */
 int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x,
                  qtt_train** out);                                            /* tt.py:434 (policy=None) */
-/* ||Ax - f|| / ||f||; exact != 0 forces the QR-sweep norm of the explicit difference
- * train; otherwise the Kronecker Gram path is used when it is provably accurate. */
+/* ||Ax - f|| / ||f||.  method 0: the reference's QR-sweep norm of the difference train
+ * (Kronecker-structured cores + blocked Householder QR); method 1: diagnostic Gram
+ * estimate (fast, loses digits when ||A|| ||x|| >> ||Ax - f||). */
 int qtt_residual_norm(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, const qtt_train* f,
-                      int exact, double* out, int* used_gram);               /* amen.py:87 */
+                      int method, double* out, int* used_gram);              /* amen.py:87 */
 
 /* ---- dense factorizations of the sweep, host buffers --------------------------- */
 /* thin QR, numpy.linalg.qr conventions: q (rows x k), r (k x cols), k = min(rows, cols) */

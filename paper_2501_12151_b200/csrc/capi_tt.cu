@@ -177,13 +177,12 @@ int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train
 }
 
 int qtt_residual_norm(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, const qtt_train* f,
-                      int exact, double* out, int* used_gram) {
+                      int method, double* out, int* used_gram) {
   return guarded([&] {
     qtt::Ctx& c = C(ctx);
-    bool gram = false;
-    if (exact) *out = qtt::residual_norm_exact(c, T(A), T(x), T(f));
-    else *out = qtt::residual_norm(c, T(A), T(x), T(f), &gram);
-    if (used_gram) *used_gram = gram ? 1 : 0;
+    if (method == 1) *out = qtt::residual_norm_gram(c, T(A), T(x), T(f));
+    else *out = qtt::residual_norm(c, T(A), T(x), T(f), nullptr);
+    if (used_gram) *used_gram = method == 1 ? 1 : 0;
   });
 }
 

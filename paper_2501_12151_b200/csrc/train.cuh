@@ -68,6 +68,8 @@ Train tt_zero(Ctx& c, const std::vector<int>& dims);
 double residual_norm(Ctx& c, const Train& A, const Train& x, const Train& f, bool* used_gram = nullptr);
 // Exact path: tt_norm(tt_sub(tt_apply(A, x), f)) via the QR sweep.
 double residual_norm_exact(Ctx& c, const Train& A, const Train& x, const Train& f);
+// Diagnostic Gram estimate (fast, loses digits when ||A|| ||x|| >> ||Ax - f||).
+double residual_norm_gram(Ctx& c, const Train& A, const Train& x, const Train& f);
 
 // Rank rule of tt.py:386-393, bit-for-bit given the same singular values.
 int rank_for_tolerance(const double* s, int n, double delta);
