@@ -318,7 +318,7 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     int S3 = 1, ktp = 1;
     cg_fused_plan(L.lb, L.m, L.rb, L.R1, L.rk, grid, S3, ktp);
     DBuf t1((long long)L.lb * L.lo * L.n * L.rk, c_.stream), t2((long long)L.lb * L.m * L.R1 * L.rk, c_.stream);
-    DBuf part3((long long)S3 * dim, c_.stream), red(2LL * grid, c_.stream);
+    DBuf part3((long long)S3 * dim, c_.stream), red(4LL * grid, c_.stream);
     CGFusedArgs a{};
     a.phil = L.phil; a.lb = L.lb; a.lo = L.lo; a.lk = L.lk;
     a.Ap = L.Ap; a.m = L.m; a.n = L.n; a.R1 = L.R1;
@@ -330,7 +330,18 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     a.out_rnorm = c_.scal + 20;
     a.out_mv_ns = (unsigned long long*)(c_.scal + 21);
     QTT_CUDA(cudaMemsetAsync(c_.scal + 21, 0, 8, c_.stream));
+    static const bool dbg = std::getenv("QTT_DEBUG") != nullptr;
+    a.phase_ns = dbg ? (unsigned long long*)(c_.scal + 32) : nullptr;
+    if (dbg) QTT_CUDA(cudaMemsetAsync(c_.scal + 32, 0, 6 * 8, c_.stream));
     cg_fused_launch(a, grid, c_.stream);
+    if (dbg) {
+      unsigned long long ph[6];
+      QTT_CUDA(cudaMemcpyAsync(ph, c_.scal + 32, sizeof(ph), cudaMemcpyDeviceToHost, c_.stream));
+      c_.sync();
+      std::fprintf(stderr, "[qtt] cg_fused dims %d,%d,%d R %d S3 %d grid %d: ns step1 %llu step2 %llu step3 %llu "
+                   "red %llu upd %llu pupd %llu\n", L.lb, L.m, L.rb, L.R1, S3, grid, ph[0], ph[1], ph[2], ph[3],
+                   ph[4], ph[5]);
+    }
     double* pin = c_.host_scalars(2);
     QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 21, 8, cudaMemcpyDeviceToHost, c_.stream));
     QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 8, 4, cudaMemcpyDeviceToHost, c_.stream));

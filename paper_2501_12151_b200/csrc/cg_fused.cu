@@ -95,21 +95,33 @@ __device__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b
 
 // q = A v  for the local operator, leaves q = sum of the split-K partials of step 3
 // unreduced in a.part3; returns after a grid barrier.
-__device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* smem, cg::grid_group& grid) {
+__device__ __forceinline__ void phase_mark(const CGFusedArgs& a, int ph, unsigned long long& t) {
+  if (a.phase_ns != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long now = gtimer();
+    a.phase_ns[ph] += now - t;
+    t = now;
+  }
+}
+
+__device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* smem, cg::grid_group& grid,
+                              unsigned long long& tp) {
   // step 1: t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
   tile::Operands o1{a.phil, a.lk, 1, v, (long long)a.n * a.rk, 1, a.lb * a.lo, a.n * a.rk, a.lk};
   phase_gemm(o1, 0, 0, 1, a.t1, (long long)a.n * a.rk, 0, 1, (o1.K + CF::BK - 1) / CF::BK, 0, smem);
   grid.sync();
+  phase_mark(a, 0, tp);
   // step 2: per X: t2[X][(m,b),V] = Ap[(m,b),(a,n)] @ t1[X][(a,n),V]
   tile::Operands o2{a.Ap, (long long)a.lo * a.n, 1, a.t1, a.rk, 1, a.m * a.R1, a.rk, a.lo * a.n};
   phase_gemm(o2, 0, (long long)a.lo * a.n * a.rk, a.lb, a.t2, a.rk, (long long)a.m * a.R1 * a.rk, 1,
              (o2.K + CF::BK - 1) / CF::BK, 0, smem);
   grid.sync();
+  phase_mark(a, 1, tp);
   // step 3 (split-K): part3[s][(X,m),Y] = t2[(X,m),(b,V)] @ phir[Y,(b,V)]^T
   tile::Operands o3{a.t2, (long long)a.R1 * a.rk, 1, a.phir, 1, (long long)a.R1 * a.rk, a.lb * a.m, a.rb,
                     a.R1 * a.rk};
   phase_gemm(o3, 0, 0, 1, a.part3, a.rb, 0, a.S3, a.kt_per3, (long long)a.lb * a.m * a.rb, smem);
   grid.sync();
+  phase_mark(a, 2, tp);
 }
 
 __device__ __forceinline__ double reduce_q(const CGFusedArgs& a, long long e) {
@@ -119,7 +131,7 @@ __device__ __forceinline__ double reduce_q(const CGFusedArgs& a, long long e) {
   return s;
 }
 
-__global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
+__global__ void __launch_bounds__(NT, 2) cg_fused_kernel(CGFusedArgs a) {
   extern __shared__ double smem[];
   __shared__ double red[24];
   cg::grid_group grid = cg::this_grid();
@@ -127,13 +139,13 @@ __global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
   // contiguous slice of the vectors owned by this CTA
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   const long long e0 = blockIdx.x * per, e1 = min(n, e0 + per);
-  unsigned long long mv_ns = 0, t0;
+  unsigned long long mv_ns = 0, t0 = 0, tp = gtimer();
   const bool timer = (blockIdx.x == 0 && threadIdx.x == 0);
 
   // ---- r = b - A x0 (only when x0 has a nonzero entry, as scipy's `x.any()`)
   if (a.xany) {
     if (timer) t0 = gtimer();
-    matvec_phases(a, a.x, smem, grid);
+    matvec_phases(a, a.x, smem, grid, tp);
     if (timer) mv_ns += gtimer() - t0;
   }
   double rr = 0.0, rz = 0.0;
@@ -152,12 +164,13 @@ __global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
   grid_sum2(a.red, gridDim.x, rr, rz, red);
   double rho = rz, rnorm = sqrt(rr);
   int it = 0;
-  grid.sync();  // everyone has read red[] before it is reused
+  // p.q partials go to a second buffer, so no extra barrier is needed before reuse
+  double* red_pq = a.red + 2 * gridDim.x;
 
   while (!(rnorm < a.atol) && it < a.maxiter) {
     // ---- q = A p
     if (timer) t0 = gtimer();
-    matvec_phases(a, a.p, smem, grid);
+    matvec_phases(a, a.p, smem, grid, tp);
     // ---- reduce q, p.q
     double pq = 0.0, dummy = 0.0;
     for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
@@ -166,12 +179,12 @@ __global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
       pq += __ldcg(a.p + e) * qi;
     }
     block_sum2(pq, dummy, red);
-    if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = pq; a.red[2 * blockIdx.x + 1] = 0.0; }
+    if (threadIdx.x == 0) { red_pq[2 * blockIdx.x] = pq; red_pq[2 * blockIdx.x + 1] = 0.0; }
     grid.sync();
+    phase_mark(a, 3, tp);
     if (timer) mv_ns += gtimer() - t0;
-    grid_sum2(a.red, gridDim.x, pq, dummy, red);
+    grid_sum2(red_pq, gridDim.x, pq, dummy, red);
     const double alpha = rho / pq;
-    grid.sync();
     // ---- x += alpha p; r -= alpha q; z = M^-1 r; rr, rz
     rr = 0.0;
     rz = 0.0;
@@ -188,6 +201,7 @@ __global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
     block_sum2(rr, rz, red);
     if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = rr; a.red[2 * blockIdx.x + 1] = rz; }
     grid.sync();
+    phase_mark(a, 4, tp);
     grid_sum2(a.red, gridDim.x, rr, rz, red);
     ++it;
     rnorm = sqrt(rr);
@@ -196,6 +210,7 @@ __global__ void __launch_bounds__(NT) cg_fused_kernel(CGFusedArgs a) {
     rho = rz;
     for (long long e = e0 + threadIdx.x; e < e1; e += NT) a.p[e] = a.z[e] + beta * a.p[e];
     grid.sync();
+    phase_mark(a, 5, tp);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *a.out_iters = it;
@@ -221,7 +236,8 @@ void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int
   const int M3 = lb * m, N3 = rb, K3 = R1 * rk;
   const int tiles = cdiv(M3, CF::BM) * cdiv(N3, CF::BN);
   const int ktiles = cdiv(K3, CF::BK);
-  int want = std::max(1, std::min(cdiv(grid, tiles), std::max(1, ktiles / 4)));
+  // as many K slices as fit in one wave of the grid (no second round of tiles)
+  int want = std::max(1, std::min(grid / std::max(1, tiles), std::max(1, ktiles / 4)));
   kt_per3 = cdiv(ktiles, want);
   S3 = cdiv(ktiles, kt_per3);
 }

@@ -22,7 +22,7 @@ struct CGFusedArgs {
   double* t2;     // lb*m*R1*rk
   double* part3;  // S3*dim split-K partials of step 3
   int S3, kt_per3;
-  double* red;  // 2*grid doubles
+  double* red;  // 4*grid doubles (two partial-sum buffers)
   long long dim;
   double atol;
   int maxiter;
@@ -31,6 +31,8 @@ struct CGFusedArgs {
   int* out_iters;
   double* out_rnorm;
   unsigned long long* out_mv_ns;  // accumulated wall ns spent in the local matvecs
+  // optional (QTT_DEBUG): wall ns per phase [step1, step2, step3, reduce+p.q, update, p-update]
+  unsigned long long* phase_ns;
 };
 
 int cg_fused_grid(int device);
