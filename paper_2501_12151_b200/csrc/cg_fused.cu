@@ -74,23 +74,38 @@ __device__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b
   const int ktiles = (o0.K + CF::BK - 1) / CF::BK;
   const long long per_batch = (long long)tm * tn * splits;
   const long long items = per_batch * batch;
-  for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-    const int b = (int)(it / per_batch);
+  // this CTA's items: blockIdx.x, +gridDim.x, ... streamed through one cp.async ring
+  const int mine = items > blockIdx.x ? (int)((items - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto decode = [&](int i, int& b, int& s) {
+    const long long it = blockIdx.x + (long long)i * gridDim.x;
+    b = (int)(it / per_batch);
     long long rem = it % per_batch;
-    const int s = (int)(rem % splits);
+    s = (int)(rem % splits);
     rem /= splits;
-    const int ti = (int)(rem / tn), tj = (int)(rem % tn);
-    tile::Operands o = o0;
-    o.A += b * a_bs;
-    o.B += b * b_bs;
-    double acc[CF::MI][CF::NI][2];
-    tile::zero_acc<CF>(acc);
-    const int k0 = s * kt_per, k1 = min(ktiles, k0 + kt_per);
-    tile::mma_tile<CF>(o, ti * CF::BM, tj * CF::BN, k0, k1, smem, acc);
+    return rem;
+  };
+  auto get = [&](int i) {
+    int b, s;
+    const long long rem = decode(i, b, s);
+    tile::TileItem t;
+    t.o = o0;
+    t.o.A += b * a_bs;
+    t.o.B += b * b_bs;
+    t.m0 = (int)(rem / tn) * CF::BM;
+    t.n0 = (int)(rem % tn) * CF::BN;
+    t.kb = s * kt_per;
+    t.ke = min(ktiles, t.kb + kt_per);
+    return t;
+  };
+  int cur = 0;
+  auto epi = [&](const tile::TileItem& t, const double (&acc)[CF::MI][CF::NI][2]) {
+    int b, s;
+    decode(cur++, b, s);
     double* Cb = C + b * c_bs + s * split_stride;
-    tile::for_each_acc<CF>(ti * CF::BM, tj * CF::BN, o.M, o.N, acc,
+    tile::for_each_acc<CF>(t.m0, t.n0, t.o.M, t.o.N, acc,
                            [&](int r, int c, double v) { Cb[(long long)r * c_rs + c] = v; });
-  }
+  };
+  tile::mma_stream<CF>(mine, get, epi, smem);
 }
 
 // q = A v  for the local operator, leaves q = sum of the split-K partials of step 3

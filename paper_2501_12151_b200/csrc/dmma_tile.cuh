@@ -134,6 +134,121 @@ __device__ __forceinline__ void mma_tile(const Operands& o, int m0, int n0, int 
   __syncthreads();  // the ring may be reused by the caller's next tile
 }
 
+template <class C>
+__device__ __forceinline__ void zero_acc_impl(double (&acc)[C::MI][C::NI][2]) {
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// One unit of a CTA's work list: output tile (m0, n0) of operands o over k-tiles [kb, ke).
+struct TileItem {
+  Operands o;
+  int m0, n0, kb, ke;
+};
+
+// Issue the cp.async copies of k-tile kt of item it into ring stage `stage`.
+template <class C>
+__device__ __forceinline__ void load_stage(const TileItem& it, int kt, int stage, double* smem) {
+  constexpr int NT = C::NT, LDA = C::LDA, LDB = C::LDB, BK = C::BK, BM = C::BM, BN = C::BN;
+  double* dA = smem + stage * BK * LDA;
+  double* dB = smem + C::STAGES * BK * LDA + stage * BK * LDB;
+  const Operands& o = it.o;
+  const bool a_mc = (o.a_rs == 1), b_nc = (o.b_cs == 1);
+  const int k0 = kt * BK;
+#pragma unroll
+  for (int i = 0; i < (BM * BK) / NT; ++i) {
+    int kk, mm;
+    tile_coord<BK, BM>(threadIdx.x + i * NT, a_mc, kk, mm);
+    const int gm = it.m0 + mm, gk = k0 + kk;
+    const bool ok = gm < o.M && gk < o.K;
+    const double* src = ok ? o.A + (long long)gm * o.a_rs + (long long)gk * o.a_cs : o.A;
+    cp_async8(dA + kk * LDA + mm, src, ok);
+  }
+#pragma unroll
+  for (int i = 0; i < (BN * BK) / NT; ++i) {
+    int kk, nn;
+    tile_coord<BK, BN>(threadIdx.x + i * NT, b_nc, kk, nn);
+    const int gn = it.n0 + nn, gk = k0 + kk;
+    const bool ok = gn < o.N && gk < o.K;
+    const double* src = ok ? o.B + (long long)gk * o.b_rs + (long long)gn * o.b_cs : o.B;
+    cp_async8(dB + kk * LDB + nn, src, ok);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void compute_stage(int stage, const double* smem, double (&acc)[C::MI][C::NI][2]) {
+  constexpr int LDA = C::LDA, LDB = C::LDB, BK = C::BK;
+  const double* cA = smem + stage * BK * LDA;
+  const double* cB = smem + C::STAGES * BK * LDA + stage * BK * LDB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp % C::WARPS_M) * C::WTM;
+  const int wn0 = (warp / C::WARPS_M) * C::WTN;
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < BK; ks += 4) {
+    double af[C::MI], bf[C::NI];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) af[i] = cA[(ks + lc) * LDA + wm0 + i * 8 + lr];
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) bf[j] = cB[(ks + lc) * LDB + wn0 + j * 8 + lr];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) dmma(acc[i][j], af[i], bf[j]);
+  }
+}
+
+// Persistent work stream: all k-tiles of the CTA's items (get(0..n-1)) flow through
+// ONE cp.async ring, so the loads of item i+1 are in flight while item i finishes and
+// its epilogue epi(item, acc) stores -- no pipeline refill bubble per tile.
+template <class C, class Get, class Epi>
+__device__ __forceinline__ void mma_stream(int n_items, Get get, Epi epi, double* smem) {
+  if (n_items <= 0) return;
+  constexpr int STAGES = C::STAGES;
+  int li = 0;
+  TileItem L = get(0);
+  int lk = L.kb;
+  auto next_load = [&](int stage) {
+    if (li >= n_items) return;
+    load_stage<C>(L, lk, stage, smem);
+    if (++lk >= L.ke) {
+      if (++li < n_items) {
+        L = get(li);
+        lk = L.kb;
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    next_load(s);
+    cp_async_commit();
+  }
+  int ci = 0;
+  TileItem Cur = get(0);
+  int ck = Cur.kb;
+  double acc[C::MI][C::NI][2];
+  zero_acc_impl<C>(acc);
+  for (int step = 0; ci < n_items; ++step) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    next_load((step + STAGES - 1) % STAGES);
+    cp_async_commit();
+    compute_stage<C>(step % STAGES, smem, acc);
+    if (++ck >= Cur.ke) {
+      epi(Cur, acc);
+      zero_acc_impl<C>(acc);
+      if (++ci < n_items) {
+        Cur = get(ci);
+        ck = Cur.kb;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
 // Visit every accumulator element: f(row, col, value) for in-range entries.
 template <class C, class F>
 __device__ __forceinline__ void for_each_acc(int m0, int n0, int M, int N, const double (&acc)[C::MI][C::NI][2],

@@ -102,8 +102,10 @@ Plan plan_for(const GemmArgs& g) {
   const long long tiles = (long long)cdiv(g.M, bm) * cdiv(g.N, bn) * batch;
   const int ktiles = cdiv(g.K, 16);
   p.kt_per = ktiles;
-  if (batch == 1 && tiles < kSMs && ktiles >= 16) {
-    int want = (int)std::min<long long>(cdiv(2 * kSMs, tiles), ktiles / 8);
+  // Long-K products with too few output tiles to fill ~2 waves are split along K
+  // (fixed-order reduction), keeping >= 8 k-tiles per slice.
+  if (batch == 1 && tiles < 2 * kSMs && ktiles >= 16) {
+    int want = (int)std::min<long long>(cdiv(3 * kSMs, tiles), ktiles / 8);
     if (want > 1) {
       p.kt_per = cdiv(ktiles, want);
       p.splits = cdiv(ktiles, p.kt_per);

@@ -1,5 +1,5 @@
 // Blocked Householder QR for large unfoldings (dgeqrf-style, right-looking):
-// a cooperative panel kernel factors nb = 32 columns (LAPACK dlarfg signs), a small
+// a cooperative panel kernel factors nb = 64 columns (LAPACK dlarfg signs), a small
 // kernel forms the block reflector T (dlarft), and the trailing matrix is updated
 // with three DMMA GEMMs  C -= V (T^T (V^T C)).  Used where the single-CTA kernel of
 // linalg.cu would serialize: the rank R*r + r_f unfoldings of the residual
@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "gemm.cuh"
 #include "linalg.cuh"
@@ -19,7 +22,7 @@ namespace qtt {
 namespace {
 
 constexpr int PNT = 256;  // threads per panel CTA
-constexpr int NB = 32;    // panel width
+constexpr int NB = 64;    // panel width
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -142,16 +145,12 @@ __global__ void build_v_kernel(const double* W, long long ld, int j0, int mrows,
 __global__ void build_t_kernel(const double* Gram, const double* tau, int jb, double* T) {
   // T[j][j] = tau_j;  T[0:j, j] = -tau_j T[0:j, 0:j] Gram[0:j, j]
   __shared__ double s[NB][NB + 1];
-  __shared__ double g[NB][NB + 1];
-  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
-    g[e / jb][e % jb] = Gram[e];
-    s[e / jb][e % jb] = 0.0;
-  }
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) s[e / jb][e % jb] = 0.0;
   __syncthreads();
   for (int j = 0; j < jb; ++j) {
     if (threadIdx.x < j) {
       double acc = 0.0;
-      for (int p = threadIdx.x; p < j; ++p) acc += s[threadIdx.x][p] * g[p][j];
+      for (int p = threadIdx.x; p < j; ++p) acc += s[threadIdx.x][p] * Gram[p * jb + j];
       s[threadIdx.x][j] = -tau[j] * acc;
     }
     if (threadIdx.x == 0) s[j][j] = tau[j];
@@ -160,26 +159,195 @@ __global__ void build_t_kernel(const double* Gram, const double* tau, int jb, do
   for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) T[e] = s[e / jb][e % jb];
 }
 
+// Lightweight grid barrier for a co-resident (cooperatively launched) grid:
+// generation-counting, one atomic per CTA per barrier.
+__device__ __forceinline__ void bar_grid(unsigned* count, volatile unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd((unsigned*)gen, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int SMEM_PANEL_DOUBLES = 26 * 1024;
+
+// Same factorization as panel_kernel, with each CTA's row block of the panel staged
+// in shared memory and few CTAs (<= 32) meeting at a lightweight barrier: the per
+// column work is a few smem passes, so the two exchanges per column dominate and
+// must be cheap.
+__global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a, unsigned* bar) {
+  extern __shared__ double P[];  // [jb][nloc] column-major
+  __shared__ double red[40];
+  __shared__ double sw[NB];
+  __shared__ double sbeta[NB];
+  const int G = gridDim.x;
+  const int rows = a.m - a.j0;
+  const int chunk = (rows + G - 1) / G;
+  const int r0 = a.j0 + blockIdx.x * chunk, r1 = min(a.m, r0 + chunk);
+  const int nloc = max(0, r1 - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* W = a.W;
+  const long long ld = a.ld;
+  for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
+    const int c = e / nloc, i = e % nloc;
+    P[e] = W[(long long)(a.j0 + c) * ld + r0 + i];
+  }
+  __syncthreads();
+  for (int j = 0; j < a.jb; ++j) {
+    const int rj = a.j0 + j;
+    double* v = P + j * nloc;  // local rows r0..r1
+    const int ib = max(0, rj + 1 - r0);  // first local row strictly below rj
+    double part = 0.0;
+    for (int i = ib + threadIdx.x; i < nloc; i += PNT) part += v[i] * v[i];
+    part = block_sum(part, red);
+    const bool own_rj = (rj >= r0 && rj < r1);
+    if (threadIdx.x == 0) {
+      a.red[blockIdx.x * (NB + 2)] = part;
+      a.red[blockIdx.x * (NB + 2) + NB + 1] = own_rj ? v[rj - r0] : 0.0;  // alpha
+    }
+    bar_grid(bar, bar + 1);
+    double xn = 0.0, al = 0.0;
+    for (int b = threadIdx.x; b < G; b += PNT) {
+      xn += __ldcg(a.red + b * (NB + 2));
+      al += __ldcg(a.red + b * (NB + 2) + NB + 1);
+    }
+    const double xnorm2 = block_sum(xn, red);
+    const double alpha = block_sum(al, red);  // exactly one CTA contributed
+    double t = 0.0, beta = alpha, scal = 1.0;
+    if (xnorm2 > 0.0) {  // dlarfg
+      beta = -copysign(hypot(alpha, sqrt(xnorm2)), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      for (int i = ib + threadIdx.x; i < nloc; i += PNT) v[i] *= scal;
+    }
+    if (threadIdx.x == 0) sbeta[j] = beta;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.tau[rj] = t;
+    __syncthreads();
+    const int nrem = a.jb - j - 1;
+    if (t != 0.0 && nrem > 0) {
+      for (int cc = warp; cc < nrem; cc += PNT / 32) {
+        const double* wc = P + (j + 1 + cc) * nloc;
+        double s = 0.0;
+        for (int i = ib + lane; i < nloc; i += 32) s += v[i] * wc[i];
+        s = warp_sum(s);
+        if (lane == 0) a.red[blockIdx.x * (NB + 2) + 1 + cc] = s + (own_rj ? wc[rj - r0] : 0.0);
+      }
+    }
+    bar_grid(bar, bar + 1);
+    if (t != 0.0 && nrem > 0) {
+      for (int cc = warp; cc < nrem; cc += PNT / 32) {
+        double s = 0.0;
+        for (int b = lane; b < G; b += 32) s += __ldcg(a.red + b * (NB + 2) + 1 + cc);
+        s = warp_sum(s);
+        if (lane == 0) sw[cc] = s * t;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < nrem * nloc; e += PNT) {
+        const int cc = e / nloc, i = e % nloc;
+        double* wc = P + (j + 1 + cc) * nloc;
+        if (i >= ib) wc[i] -= sw[cc] * v[i];
+        else if (own_rj && i == rj - r0) wc[i] -= sw[cc];
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.jb; j += PNT) {
+    const int rj = a.j0 + j;
+    if (rj >= r0 && rj < r1) P[j * nloc + (rj - r0)] = sbeta[j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
+    const int c = e / nloc, i = e % nloc;
+    W[(long long)(a.j0 + c) * ld + r0 + i] = P[e];
+  }
+}
+
 int panel_grid(int rows) {
   // enough CTAs that each owns >= ~256 rows, capped at one wave
   return std::max(1, std::min(128, (rows + 255) / 256));
 }
 
+// CTAs for the shared-memory panel: each row block must fit SMEM_PANEL_DOUBLES.
+int panel_smem_grid(int rows, int jb) {
+  const int max_rows = SMEM_PANEL_DOUBLES / std::max(1, jb);
+  return std::max(1, (rows + max_rows - 1) / max_rows);
+}
+
 }  // namespace
+
+// QTT_DEBUG: per-stage CUDA-event timing of the blocked QR, printed per call.
+struct QrTimer {
+  bool on;
+  cudaStream_t s;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> stage;
+  double ms[6] = {0, 0, 0, 0, 0, 0};
+  explicit QrTimer(cudaStream_t st) : on(std::getenv("QTT_DEBUG") != nullptr), s(st) {}
+  void mark(int st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    stage.push_back(st);
+  }
+  void report(int m, int n) {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back());
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev[i - 1], ev[i]);
+      ms[stage[i]] += t;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    std::fprintf(stderr, "[qtt] geqrf %dx%d ms: panel %.2f v+gram+T %.2f Y1 %.2f Y2 %.2f update %.2f\n", m, n,
+                 ms[1], ms[2], ms[3], ms[4], ms[5]);
+  }
+};
 
 void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
   const int k = std::min(m, n);
-  DBuf red(129LL * (NB + 1), c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
-      T(NB * NB, c.stream), Y1, Y2;
+  QrTimer tm(c.stream);
+  tm.mark(0);
+  DBuf red(149LL * (NB + 2), c.stream), bar(1, c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
+      T(NB * NB, c.stream), Y1, Y2, Wsk;
   const long long ld = m;
+  QTT_CUDA(cudaMemsetAsync(bar.p, 0, 8, c.stream));  // barrier counter + generation
   for (int j0 = 0; j0 < k; j0 += NB) {
     const int jb = std::min(NB, k - j0);
     const int mrows = m - j0;
     PanelArgs pa{W, ld, m, j0, jb, tau, red.p};
-    const int G = panel_grid(mrows);
-    void* args[] = {(void*)&pa};
-    QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PNT), args, 0, c.stream));
+    const int Gs = panel_smem_grid(mrows, jb);
+    if (Gs <= 148) {
+      static bool attr = false;
+      if (!attr) {
+        QTT_CUDA(cudaFuncSetAttribute(panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_PANEL_DOUBLES * 8));
+        attr = true;
+      }
+      const int chunk = (mrows + Gs - 1) / Gs;
+      unsigned* barp = (unsigned*)bar.p;
+      void* args[] = {(void*)&pa, (void*)&barp};
+      QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_smem_kernel, dim3(Gs), dim3(PNT), args,
+                                           (size_t)chunk * jb * 8, c.stream));
+    } else {
+      const int G = panel_grid(mrows);
+      void* args[] = {(void*)&pa};
+      QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PNT), args, 0, c.stream));
+    }
     QTT_CHECK_LAUNCH();
+    tm.mark(1);
     const int n2 = n - j0 - jb;
     if (n2 <= 0) continue;
     build_v_kernel<<<std::min(1184, cdiv((long long)mrows * jb, 256)), 256, 0, c.stream>>>(W, ld, j0, mrows,
@@ -191,10 +359,13 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       g.A = Vb.p; g.a_rs = mrows; g.a_cs = 1;
       g.B = Vb.p; g.b_rs = 1; g.b_cs = mrows;
       gemm_set_C(g, Gram.p, jb);
-      gemm(g, c.stream);
+      const long long need = gemm_workspace_hint(g);  // one output tile, K = mrows: split K
+      if (Wsk.n < need) Wsk.alloc(need, c.stream);
+      gemm(g, c.stream, Wsk.p, Wsk.n);
     }
     build_t_kernel<<<1, NB, 0, c.stream>>>(Gram.p, tau + j0, jb, T.p);
     QTT_CHECK_LAUNCH();
+    tm.mark(2);
     if (Y1.n < (long long)jb * n2) Y1.alloc((long long)jb * n2, c.stream);
     if (Y2.n < (long long)jb * n2) Y2.alloc((long long)jb * n2, c.stream);
     double* C = W + (long long)(j0 + jb) * ld + j0;
@@ -205,9 +376,10 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       g.B = C; g.b_rs = 1; g.b_cs = ld;
       gemm_set_C(g, Y1.p, n2);
       const long long need = gemm_workspace_hint(g);
-      DBuf ws(need, c.stream);
-      gemm(g, c.stream, ws.p, ws.n);
+      if (Wsk.n < need) Wsk.alloc(need, c.stream);
+      gemm(g, c.stream, Wsk.p, Wsk.n);
     }
+    tm.mark(3);
     {  // Y2 = T^T Y1
       GemmArgs g;
       g.M = jb; g.N = n2; g.K = jb;
@@ -216,6 +388,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       gemm_set_C(g, Y2.p, n2);
       gemm(g, c.stream);
     }
+    tm.mark(4);
     {  // C -= Vb Y2
       GemmArgs g;
       g.M = mrows; g.N = n2; g.K = jb;
@@ -225,7 +398,9 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       g.alpha = -1.0; g.beta = 1.0;
       gemm(g, c.stream);
     }
+    tm.mark(5);
   }
+  tm.report(m, n);
 }
 
 }  // namespace qtt
