@@ -1,6 +1,8 @@
 // Dense FP64 kernels of the sweep (see linalg.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "linalg.cuh"
@@ -127,15 +129,18 @@ __global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView
 // Outputs (sorted by descending norm): U = W/sigma (m x n view), s, Vt (n x n view).
 template <int NT>
 __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, double* so, MatView Vto,
-                                                    double* gws, int use_smem, double tol) {
+                                                    double* gws, int use_smem, double tol, int dbg) {
   extern __shared__ double sm[];
   __shared__ int s_rot;
+  int sweeps_done = 0;
   const int m = in.rows, n = in.cols;
   double* W = use_smem ? sm : gws;                      // m x n, column-major
   double* V = W + (long long)m * n;                     // n x n, column-major
   double* sig = V + (long long)n * n;                   // n
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
+  constexpr int GS = 8;  // lanes per column pair
+  const int gl = tid % GS;
 
   for (long long e = tid; e < (long long)m * n; e += NT) {
     const int i = (int)(e % m), j = (int)(e / m);
@@ -149,43 +154,54 @@ __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, dou
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int r = 0; r < P - 1; ++r) {
-      for (int q = warp; q < P / 2; q += NW) {
-        int a, b;
+      // GS lanes per column pair: all n/2 pairs of a round run concurrently
+      // warp-uniform trip count (the shuffles below need all 32 lanes)
+      for (int qb = warp * (32 / GS); qb < P / 2; qb += NT / GS) {
+        const int q = qb + lane / GS;
+        int a = 0, b = 0;
         if (q == 0) { a = r; b = P - 1; }
         else { a = (r + q) % (P - 1); b = (r - q + (P - 1)) % (P - 1); }
-        if (a >= n || b >= n) continue;
+        const bool live = q < P / 2 && a < n && b < n;
         if (a > b) { const int t = a; a = b; b = t; }
+        double al = 0, be = 0, ga = 0;
         double* wa = W + (long long)a * m;
         double* wb = W + (long long)b * m;
-        double al = 0, be = 0, ga = 0;
-        for (int i = lane; i < m; i += 32) {
-          const double x = wa[i], y = wb[i];
-          al += x * x; be += y * y; ga += x * y;
+        if (live)
+          for (int i = gl; i < m; i += GS) {
+            const double x = wa[i], y = wb[i];
+            al += x * x; be += y * y; ga += x * y;
+          }
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (ga == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        if (!live || ga == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = lane; i < m; i += 32) {
+        for (int i = gl; i < m; i += GS) {
           const double x = wa[i], y = wb[i];
           wa[i] = cs * x - sn * y;
           wb[i] = sn * x + cs * y;
         }
         double* va = V + (long long)a * n;
         double* vb = V + (long long)b * n;
-        for (int i = lane; i < n; i += 32) {
+        for (int i = gl; i < n; i += GS) {
           const double x = va[i], y = vb[i];
           va[i] = cs * x - sn * y;
           vb[i] = sn * x + cs * y;
         }
-        if (lane == 0) s_rot = 1;
+        if (gl == 0) s_rot = 1;
       }
       __syncthreads();
     }
+    sweeps_done = sweep + 1;
     if (!s_rot) break;
     __syncthreads();
   }
+  if (dbg && tid == 0) printf("[qtt] jacobi %dx%d sweeps %d\n", m, n, sweeps_done);
   // column norms
   for (int c = warp; c < n; c += NW) {
     const double* wc = W + (long long)c * m;
@@ -484,10 +500,15 @@ void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
   }
 }
 
+static int jacobi_dbg() {
+  static const int on = std::getenv("QTT_DEBUG_JACOBI") != nullptr;
+  return on;
+}
+
 static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   const int m = in.rows, n = in.cols;
   const long long need = (long long)m * n + (long long)n * n + n;
-  constexpr int NT = 512;
+  constexpr int NT = 1024;
   const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
   if (need <= kSmemDoubles) {
     static bool attr = false;
@@ -496,11 +517,11 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
                                     kSmemDoubles * 8));
       attr = true;
     }
-    jacobi_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, U, s, Vt, nullptr, 1, tol);
+    jacobi_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, U, s, Vt, nullptr, 1, tol, jacobi_dbg());
     QTT_CHECK_LAUNCH();
   } else {
     DBuf ws(need, c.stream);
-    jacobi_kernel<NT><<<1, NT, 0, c.stream>>>(in, U, s, Vt, ws.p, 0, tol);
+    jacobi_kernel<NT><<<1, NT, 0, c.stream>>>(in, U, s, Vt, ws.p, 0, tol, jacobi_dbg());
     QTT_CHECK_LAUNCH();
   }
 }
