@@ -261,8 +261,19 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     if (prm_.fused_cg) {  // one cooperative kernel: row sums + Cholesky + both solves
       QTT_CUDA(cudaMemsetAsync(c_.scal + 8, 0, 8, c_.stream));
       QTT_CUDA(cudaMemsetAsync(c_.flags + 3, 0, 4, c_.stream));
-      CholArgs ca{M.p, (int)dim, dim, u.p, c_.scal + 8, c_.flags + 3};
+      DBuf Linv(chol_fused_linv_doubles((int)dim), c_.stream), ywork(dim, c_.stream);
+      static const bool dbg = std::getenv("QTT_DEBUG") != nullptr;
+      CholArgs ca{M.p, (int)dim, dim, u.p, c_.scal + 8, c_.flags + 3, Linv.p, ywork.p,
+                  dbg ? (unsigned long long*)(c_.scal + 40) : nullptr};
+      if (dbg) QTT_CUDA(cudaMemsetAsync(c_.scal + 40, 0, 6 * 8, c_.stream));
       chol_fused_launch(ca, chol_fused_grid(c_.device), c_.stream);
+      if (dbg) {
+        unsigned long long ph[6];
+        QTT_CUDA(cudaMemcpyAsync(ph, c_.scal + 40, sizeof(ph), cudaMemcpyDeviceToHost, c_.stream));
+        c_.sync();
+        std::fprintf(stderr, "[qtt] chol dim %lld ns: rowsum %llu diag %llu panel %llu trail %llu inv %llu fwd %llu\n",
+                     dim, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+      }
       c_.stats.chol_solves++;
     } else {
       max_abs_row_sum(c_, M.p, (int)dim, dim, c_.scal + 8);
