@@ -328,13 +328,23 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     const int grid = cg_fused_grid(c_.device);
     int S3 = 1, ktp = 1;
     cg_fused_plan(L.lb, L.m, L.rb, L.R1, L.rk, grid, S3, ktp);
-    DBuf t1((long long)L.lb * L.lo * L.n * L.rk, c_.stream), t2((long long)L.lb * L.m * L.R1 * L.rk, c_.stream);
+    // compose steps 1+2 into one GEMM phase when that costs at most ~15% more flops
+    // (it saves a grid barrier and a pipeline fill per matvec); QTT_CG_COMPOSE=0/1 forces
+    static const int compose_env = std::getenv("QTT_CG_COMPOSE") ? std::atoi(std::getenv("QTT_CG_COMPOSE")) : -1;
+    const double f3 = cg_fused_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk, false);
+    const double fc = cg_fused_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk, true);
+    const bool composed = compose_env >= 0 ? compose_env != 0 : fc <= 1.15 * f3;
+    DBuf t1(composed ? 1 : (long long)L.lb * L.lo * L.n * L.rk, c_.stream),
+        t2((long long)L.lb * L.m * L.R1 * L.rk, c_.stream);
+    DBuf bop(composed ? (long long)L.lb * L.m * L.R1 * L.lk * L.n : 1, c_.stream);
+    if (composed) cg_fused_build_bop(L.phil, L.lb, L.lo, L.lk, L.Ap, L.m, L.n, L.R1, bop.p, c_.stream);
     DBuf part3((long long)S3 * dim, c_.stream), red(4LL * grid, c_.stream);
     CGFusedArgs a{};
     a.phil = L.phil; a.lb = L.lb; a.lo = L.lo; a.lk = L.lk;
     a.Ap = L.Ap; a.m = L.m; a.n = L.n; a.R1 = L.R1;
     a.phir = L.phir; a.rb = L.rb; a.rk = L.rk;
     a.b = rhs_p; a.invd = invd.p; a.x = u.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
+    a.Bop = composed ? bop.p : nullptr;
     a.t1 = t1.p; a.t2 = t2.p; a.part3 = part3.p; a.S3 = S3; a.kt_per3 = ktp; a.red = red.p;
     a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;
     a.out_iters = c_.flags + 8;

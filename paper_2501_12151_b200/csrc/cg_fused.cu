@@ -12,6 +12,7 @@
 
 #include "cg_fused.cuh"
 #include "dmma_tile.cuh"
+#include "gemm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -120,6 +121,14 @@ __device__ __forceinline__ void phase_mark(const CGFusedArgs& a, int ph, unsigne
 
 __device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* smem, cg::grid_group& grid,
                               unsigned long long& tp) {
+  if (a.Bop != nullptr) {
+    // steps 1+2 composed: per X: t2[X][(m,b),V] = Bop[X][(m,b),(U,n)] @ v[(U,n),V]
+    tile::Operands oc{a.Bop, (long long)a.lk * a.n, 1, v, a.rk, 1, a.m * a.R1, a.rk, a.lk * a.n};
+    phase_gemm(oc, (long long)a.m * a.R1 * a.lk * a.n, 0, a.lb, a.t2, a.rk, (long long)a.m * a.R1 * a.rk, 1,
+               (oc.K + CF::BK - 1) / CF::BK, 0, smem);
+    grid.sync();
+    phase_mark(a, 1, tp);
+  } else {
   // step 1: t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
   tile::Operands o1{a.phil, a.lk, 1, v, (long long)a.n * a.rk, 1, a.lb * a.lo, a.n * a.rk, a.lk};
   phase_gemm(o1, 0, 0, 1, a.t1, (long long)a.n * a.rk, 0, 1, (o1.K + CF::BK - 1) / CF::BK, 0, smem);
@@ -131,6 +140,7 @@ __device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* sme
              (o2.K + CF::BK - 1) / CF::BK, 0, smem);
   grid.sync();
   phase_mark(a, 1, tp);
+  }
   // step 3 (split-K): part3[s][(X,m),Y] = t2[(X,m),(b,V)] @ phir[Y,(b,V)]^T
   tile::Operands o3{a.t2, (long long)a.R1 * a.rk, 1, a.phir, 1, (long long)a.R1 * a.rk, a.lb * a.m, a.rb,
                     a.R1 * a.rk};
@@ -255,6 +265,24 @@ void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int
   int want = std::max(1, std::min(grid / std::max(1, tiles), std::max(1, ktiles / 4)));
   kt_per3 = cdiv(ktiles, want);
   S3 = cdiv(ktiles, kt_per3);
+}
+
+double cg_fused_flops(int lb, int lo, int lk, int m, int n, int R1, int rb, int rk, bool composed) {
+  const double s3 = 2.0 * lb * m * rb * (double)R1 * rk;
+  if (composed) return 2.0 * lb * (double)m * R1 * lk * n * rk + s3;
+  return 2.0 * lb * (double)lo * lk * n * rk + 2.0 * lb * (double)m * R1 * lo * n * rk + s3;
+}
+
+void cg_fused_build_bop(const double* phil, int lb, int lo, int lk, const double* Ap, int m, int n, int R1,
+                        double* Bop, cudaStream_t s) {
+  // batched over (X, n'):  Bop[X][(m,b)][U][n'] = sum_a Ap[(m,b)][a][n'] phil[X][a][U]
+  GemmArgs g;
+  g.M = m * R1; g.N = lk; g.K = lo;
+  g.A = Ap; g.a_rs = (long long)lo * n; g.a_cs = n; g.a_bs1 = 0; g.a_bs2 = 1;
+  g.B = phil; g.b_rs = lk; g.b_cs = 1; g.b_bs1 = (long long)lo * lk; g.b_bs2 = 0;
+  g.C = Bop; g.c_rs = (long long)lk * n; g.c_cs = n; g.c_bs1 = (long long)m * R1 * lk * n; g.c_bs2 = 1;
+  g.batch1 = lb; g.batch2 = n;
+  gemm(g, s, nullptr, 0);
 }
 
 void cg_fused_launch(const CGFusedArgs& a, int grid, cudaStream_t s) {

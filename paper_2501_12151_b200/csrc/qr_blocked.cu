@@ -159,33 +159,14 @@ __global__ void build_t_kernel(const double* Gram, const double* tau, int jb, do
   for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) T[e] = s[e / jb][e % jb];
 }
 
-// Lightweight grid barrier for a co-resident (cooperatively launched) grid:
-// generation-counting, one atomic per CTA per barrier.
-__device__ __forceinline__ void bar_grid(unsigned* count, volatile unsigned* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd((unsigned*)gen, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 constexpr int SMEM_PANEL_DOUBLES = 26 * 1024;
 
 // Same factorization as panel_kernel, with each CTA's row block of the panel staged
-// in shared memory and few CTAs (<= 32) meeting at a lightweight barrier: the per
-// column work is a few smem passes, so the two exchanges per column dominate and
-// must be cheap.
-__global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a, unsigned* bar) {
+// in shared memory and few CTAs (<= 32): the per
+// column work is a few smem passes, so the two grid barriers per column dominate
+// (cg grid.sync measured 1.2 us vs 2.1-2.5 us for a hand-rolled generation barrier,
+// tools/barrier_bench.cu).
+__global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
   extern __shared__ double P[];  // [jb][nloc] column-major
   __shared__ double red[40];
   __shared__ double sw[NB];
@@ -215,7 +196,7 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a, unsigned* 
       a.red[blockIdx.x * (NB + 2)] = part;
       a.red[blockIdx.x * (NB + 2) + NB + 1] = own_rj ? v[rj - r0] : 0.0;  // alpha
     }
-    bar_grid(bar, bar + 1);
+    cg::this_grid().sync();
     double xn = 0.0, al = 0.0;
     for (int b = threadIdx.x; b < G; b += PNT) {
       xn += __ldcg(a.red + b * (NB + 2));
@@ -243,13 +224,16 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a, unsigned* 
         if (lane == 0) a.red[blockIdx.x * (NB + 2) + 1 + cc] = s + (own_rj ? wc[rj - r0] : 0.0);
       }
     }
-    bar_grid(bar, bar + 1);
+    cg::this_grid().sync();
     if (t != 0.0 && nrem > 0) {
-      for (int cc = warp; cc < nrem; cc += PNT / 32) {
+      {  // 4 threads per column, all partial loads in flight at once; fixed order
+        const int cc = threadIdx.x >> 2, sub = threadIdx.x & 3;
         double s = 0.0;
-        for (int b = lane; b < G; b += 32) s += __ldcg(a.red + b * (NB + 2) + 1 + cc);
-        s = warp_sum(s);
-        if (lane == 0) sw[cc] = s * t;
+        if (cc < nrem)
+          for (int b = sub; b < G; b += 4) s += __ldcg(a.red + b * (NB + 2) + 1 + cc);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (sub == 0 && cc < nrem) sw[cc] = s * t;
       }
       __syncthreads();
       for (int e = threadIdx.x; e < nrem * nloc; e += PNT) {
@@ -279,9 +263,14 @@ int panel_grid(int rows) {
 }
 
 // CTAs for the shared-memory panel: each row block must fit SMEM_PANEL_DOUBLES.
+// Small row blocks (~QTT_PANEL_ROWS rows, default 64) keep the per-column work of
+// each CTA short: the panel is latency-bound, so more CTAs beat fuller ones.
 int panel_smem_grid(int rows, int jb) {
+  static const int target = std::getenv("QTT_PANEL_ROWS") ? std::atoi(std::getenv("QTT_PANEL_ROWS")) : 64;
   const int max_rows = SMEM_PANEL_DOUBLES / std::max(1, jb);
-  return std::max(1, (rows + max_rows - 1) / max_rows);
+  const int need = std::max(1, (rows + max_rows - 1) / max_rows);
+  const int want = std::min(148, std::max(1, (rows + target - 1) / std::max(1, target)));
+  return std::max(need, want);
 }
 
 }  // namespace
@@ -320,10 +309,9 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
   const int k = std::min(m, n);
   QrTimer tm(c.stream);
   tm.mark(0);
-  DBuf red(149LL * (NB + 2), c.stream), bar(1, c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
+  DBuf red(149LL * (NB + 2), c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
       T(NB * NB, c.stream), Y1, Y2, Wsk;
   const long long ld = m;
-  QTT_CUDA(cudaMemsetAsync(bar.p, 0, 8, c.stream));  // barrier counter + generation
   for (int j0 = 0; j0 < k; j0 += NB) {
     const int jb = std::min(NB, k - j0);
     const int mrows = m - j0;
@@ -337,8 +325,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
         attr = true;
       }
       const int chunk = (mrows + Gs - 1) / Gs;
-      unsigned* barp = (unsigned*)bar.p;
-      void* args[] = {(void*)&pa, (void*)&barp};
+      void* args[] = {(void*)&pa};
       QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_smem_kernel, dim3(Gs), dim3(PNT), args,
                                            (size_t)chunk * jb * 8, c.stream));
     } else {
