@@ -8,9 +8,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "amen.cuh"
 #include "cg_fused.cuh"
+#include "cg_tma.cuh"
+#include "tma_tile.cuh"
 #include "chol_fused.cuh"
 #include "contract.cuh"
 #include "gemm.cuh"
@@ -323,11 +326,109 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
   QTT_CUDA(cudaMemcpyAsync(u.p, prev_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
   QTT_CUDA(cudaMemcpyAsync(r.p, rhs_p, dim * 8, cudaMemcpyDeviceToDevice, c_.stream));
   const double kflops = local_matvec_flops(L.lb, L.lo, L.lk, L.m, L.n, L.R1, L.rb, L.rk);
+  static const int tma_env = std::getenv("QTT_CG_TMA") ? std::atoi(std::getenv("QTT_CG_TMA")) : 1;
+  if (prm_.fused_cg && tma_env != 0 && cg_tma_supported(L.lk, L.n) && L.lb == L.lk && L.rb == L.rk &&
+      L.m == L.n) {
+    // one persistent cooperative kernel on the TMA engine (cg_tma.cu); vectors transposed
+    const int grid = cg_tma_grid(c_.device);
+    const CGTmaPlan pl = cg_tma_plan(L.lb, L.m, L.R1, L.lk, L.n, L.rb, L.rk, grid);
+    const long long K3 = (long long)L.R1 * L.rk, K3p = K3 + (K3 & 1);
+    const long long rowsA = (long long)L.lk * L.n;  // (U,n)
+    DBuf bT(dim, c_.stream), dT(dim, c_.stream), xT(dim, c_.stream);
+    transpose_2d(rhs_p, bT.p, rowsA, L.rk, c_.stream);
+    transpose_2d(invd.p, dT.p, rowsA, L.rk, c_.stream);
+    transpose_2d(prev_p, xT.p, rowsA, L.rk, c_.stream);
+    DBuf bop((long long)L.lb * L.m * L.R1 * rowsA, c_.stream);
+    cg_fused_build_bop(L.phil, L.lb, L.lo, L.lk, L.Ap, L.m, L.n, L.R1, bop.p, c_.stream);
+    DBuf phir_pad;
+    const double* phir = L.phir;
+    if (K3p != K3) {
+      phir_pad.alloc((long long)L.rb * K3p, c_.stream);
+      QTT_CUDA(cudaMemcpy2DAsync(phir_pad.p, K3p * 8, L.phir, K3 * 8, K3 * 8, L.rb, cudaMemcpyDeviceToDevice,
+                                 c_.stream));
+      phir = phir_pad.p;
+    }
+    DBuf t2((long long)L.lb * L.m * K3p, c_.stream), part3((long long)pl.S3 * dim, c_.stream);
+    DBuf red(4LL * grid, c_.stream), skws((long long)grid * cg_tma_tile_doubles(), c_.stream);
+    DBuf flagsb(cdiv(grid, 2), c_.stream);
+    CGTmaArgs a;
+    std::memset(&a, 0, sizeof(a));
+    make_tensor_map_2d(&a.map_bop, bop.p, (long long)L.lb * L.m * L.R1, rowsA, rowsA, pl.box1_a);
+    make_tensor_map_2d(&a.map_p, p.p, L.rk, rowsA, rowsA, pl.box1_b);
+    make_tensor_map_2d(&a.map_x, xT.p, L.rk, rowsA, rowsA, pl.box1_b);
+    make_tensor_map_2d(&a.map_phir, phir, L.rb, K3, K3p, pl.box2_a);
+    make_tensor_map_2d(&a.map_t2, t2.p, (long long)L.lb * L.m, K3, K3p, pl.box2_b);
+    a.lb = L.lb; a.m = L.m; a.R1 = L.R1; a.lk = L.lk; a.n = L.n; a.rb = L.rb; a.rk = L.rk; a.K3p = K3p;
+    a.cfg1 = pl.cfg1; a.cfg2 = pl.cfg2;
+    a.b = bT.p; a.invd = dT.p; a.x = xT.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
+    a.t2 = t2.p; a.part3 = part3.p; a.S3 = pl.S3; a.kt_per3 = pl.kt_per3; a.red = red.p;
+    a.sk_ws = skws.p; a.sk_flags = (unsigned*)flagsb.p;
+    a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;
+    a.out_iters = c_.flags + 8;
+    a.out_rnorm = c_.scal + 20;
+    a.out_mv_ns = (unsigned long long*)(c_.scal + 21);
+    QTT_CUDA(cudaMemsetAsync(c_.scal + 21, 0, 8, c_.stream));
+    static const bool dbg = std::getenv("QTT_DEBUG") != nullptr;
+    a.phase_ns = dbg ? (unsigned long long*)(c_.scal + 32) : nullptr;
+    if (dbg) QTT_CUDA(cudaMemsetAsync(c_.scal + 32, 0, 6 * 8, c_.stream));
+    static const bool dbg2 = std::getenv("QTT_DEBUG") && std::atoi(std::getenv("QTT_DEBUG")) >= 2;
+    DBuf ctans(dbg2 ? 3LL * grid : 1, c_.stream);
+    if (dbg2) {
+      QTT_CUDA(cudaMemsetAsync(ctans.p, 0, 24LL * grid, c_.stream));
+      a.cta_ns = (unsigned long long*)ctans.p;
+    }
+    cg_tma_launch(a, grid, c_.stream);
+    if (dbg2) {
+      std::vector<unsigned long long> h(3 * grid);
+      QTT_CUDA(cudaMemcpyAsync(h.data(), ctans.p, 24LL * grid, cudaMemcpyDeviceToHost, c_.stream));
+      c_.sync();
+      if (std::getenv("QTT_CTA_DUMP")) {
+        std::fprintf(stderr, "[qtt] cta_dump");
+        for (int i = 0; i < grid; ++i) std::fprintf(stderr, " %llu:%llu", h[2 * grid + i], h[i]);
+        std::fprintf(stderr, "\n");
+      }
+      for (int ph = 0; ph < 2; ++ph) {
+        std::vector<unsigned long long> v(h.begin() + ph * grid, h.begin() + (ph + 1) * grid);
+        std::vector<unsigned long long> srt = v;
+        std::sort(srt.begin(), srt.end());
+        int amax = (int)(std::max_element(v.begin(), v.end()) - v.begin());
+        std::fprintf(stderr, "[qtt] cg_tma phase%d per-CTA busy ns: min %llu med %llu p90 %llu max %llu (cta %d)\n",
+                     ph + 1, srt[0], srt[grid / 2], srt[grid * 9 / 10], srt[grid - 1], amax);
+      }
+    }
+    transpose_2d(xT.p, u.p, L.rk, rowsA, c_.stream);
+    double* pin = c_.host_scalars(2);
+    QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 21, 8, cudaMemcpyDeviceToHost, c_.stream));
+    QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 8, 4, cudaMemcpyDeviceToHost, c_.stream));
+    c_.sync();
+    unsigned long long ns;
+    std::memcpy(&ns, pin, 8);
+    int it;
+    std::memcpy(&it, pin + 1, 4);
+    iters = it;
+    if (dbg) {
+      unsigned long long ph[6];
+      QTT_CUDA(cudaMemcpyAsync(ph, c_.scal + 32, sizeof(ph), cudaMemcpyDeviceToHost, c_.stream));
+      c_.sync();
+      std::fprintf(stderr, "[qtt] cg_fused dims %d,%d,%d R %d S3 %d tiles %d,%d composed %d grid %d iters %d: ns "
+                   "step1 %llu step2 %llu step3 %llu red %llu upd %llu pupd %llu\n", L.lb, L.m, L.rb, L.R1, pl.S3,
+                   10 + pl.cfg1, 10 + pl.cfg2, 1, grid, it, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+    }
+    const int calls = it + (xany ? 1 : 0);
+    c_.stats.cg_iters += it;
+    c_.stats.k1_calls += calls;
+    c_.stats.k1_flops += kflops * calls;
+    if (c_.profiling) {
+      c_.stats.k1_ms += ns * 1e-6;
+      c_.stats.k1_timed_flops += kflops * calls;
+    }
+    return u;
+  }
   if (prm_.fused_cg) {
     // one persistent cooperative kernel for the whole CG solve (cg_fused.cu)
     const int grid = cg_fused_grid(c_.device);
-    int S3 = 1, ktp = 1;
-    cg_fused_plan(L.lb, L.m, L.rb, L.R1, L.rk, grid, S3, ktp);
+    int S3 = 1, ktp = 1, tileA = 0, tile3 = 0;
+    cg_fused_plan(L.lb, L.m, L.rb, L.R1, L.rk, grid, S3, ktp, tileA, tile3);
     // compose steps 1+2 into one GEMM phase when that costs at most ~15% more flops
     // (it saves a grid barrier and a pipeline fill per matvec); QTT_CG_COMPOSE=0/1 forces
     static const int compose_env = std::getenv("QTT_CG_COMPOSE") ? std::atoi(std::getenv("QTT_CG_COMPOSE")) : -1;
@@ -345,7 +446,7 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     a.phir = L.phir; a.rb = L.rb; a.rk = L.rk;
     a.b = rhs_p; a.invd = invd.p; a.x = u.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
     a.Bop = composed ? bop.p : nullptr;
-    a.t1 = t1.p; a.t2 = t2.p; a.part3 = part3.p; a.S3 = S3; a.kt_per3 = ktp; a.red = red.p;
+    a.t1 = t1.p; a.t2 = t2.p; a.part3 = part3.p; a.S3 = S3; a.kt_per3 = ktp; a.tileA = tileA; a.tile3 = tile3; a.red = red.p;
     a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;
     a.out_iters = c_.flags + 8;
     a.out_rnorm = c_.scal + 20;
@@ -355,14 +456,6 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     a.phase_ns = dbg ? (unsigned long long*)(c_.scal + 32) : nullptr;
     if (dbg) QTT_CUDA(cudaMemsetAsync(c_.scal + 32, 0, 6 * 8, c_.stream));
     cg_fused_launch(a, grid, c_.stream);
-    if (dbg) {
-      unsigned long long ph[6];
-      QTT_CUDA(cudaMemcpyAsync(ph, c_.scal + 32, sizeof(ph), cudaMemcpyDeviceToHost, c_.stream));
-      c_.sync();
-      std::fprintf(stderr, "[qtt] cg_fused dims %d,%d,%d R %d S3 %d grid %d: ns step1 %llu step2 %llu step3 %llu "
-                   "red %llu upd %llu pupd %llu\n", L.lb, L.m, L.rb, L.R1, S3, grid, ph[0], ph[1], ph[2], ph[3],
-                   ph[4], ph[5]);
-    }
     double* pin = c_.host_scalars(2);
     QTT_CUDA(cudaMemcpyAsync(pin, c_.scal + 21, 8, cudaMemcpyDeviceToHost, c_.stream));
     QTT_CUDA(cudaMemcpyAsync(pin + 1, c_.flags + 8, 4, cudaMemcpyDeviceToHost, c_.stream));
@@ -372,6 +465,14 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     int it;
     std::memcpy(&it, pin + 1, 4);
     iters = it;
+    if (dbg) {
+      unsigned long long ph[6];
+      QTT_CUDA(cudaMemcpyAsync(ph, c_.scal + 32, sizeof(ph), cudaMemcpyDeviceToHost, c_.stream));
+      c_.sync();
+      std::fprintf(stderr, "[qtt] cg_fused dims %d,%d,%d R %d S3 %d tiles %d,%d composed %d grid %d iters %d: ns "
+                   "step1 %llu step2 %llu step3 %llu red %llu upd %llu pupd %llu\n", L.lb, L.m, L.rb, L.R1, S3,
+                   tileA, tile3, composed ? 1 : 0, grid, it, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+    }
     const int calls = it + (xany ? 1 : 0);
     c_.stats.cg_iters += it;
     c_.stats.k1_calls += calls;

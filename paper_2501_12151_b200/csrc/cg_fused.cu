@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "cg_fused.cuh"
 #include "dmma_tile.cuh"
@@ -68,11 +69,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // One GEMM phase: every CTA takes work items blockIdx.x, +gridDim.x, ...
 // C[b][r*c_rs + c] = sum_k op(A_b)(r,k) op(B_b)(k,c)   (split-K when splits > 1:
 // item writes its partial into C + s*split_stride instead)
-__device__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b_bs, int batch, double* C,
+template <class T>
+__device__ __noinline__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b_bs, int batch, double* C,
                            long long c_rs, long long c_bs, int splits, int kt_per, long long split_stride,
                            double* smem) {
-  const int tm = (o0.M + CF::BM - 1) / CF::BM, tn = (o0.N + CF::BN - 1) / CF::BN;
-  const int ktiles = (o0.K + CF::BK - 1) / CF::BK;
+  const int tm = (o0.M + T::BM - 1) / T::BM, tn = (o0.N + T::BN - 1) / T::BN;
+  const int ktiles = (o0.K + T::BK - 1) / T::BK;
   const long long per_batch = (long long)tm * tn * splits;
   const long long items = per_batch * batch;
   // this CTA's items: blockIdx.x, +gridDim.x, ... streamed through one cp.async ring
@@ -92,21 +94,41 @@ __device__ void phase_gemm(const tile::Operands& o0, long long a_bs, long long b
     t.o = o0;
     t.o.A += b * a_bs;
     t.o.B += b * b_bs;
-    t.m0 = (int)(rem / tn) * CF::BM;
-    t.n0 = (int)(rem % tn) * CF::BN;
+    t.m0 = (int)(rem / tn) * T::BM;
+    t.n0 = (int)(rem % tn) * T::BN;
     t.kb = s * kt_per;
     t.ke = min(ktiles, t.kb + kt_per);
     return t;
   };
   int cur = 0;
-  auto epi = [&](const tile::TileItem& t, const double (&acc)[CF::MI][CF::NI][2]) {
+  auto epi = [&](const tile::TileItem& t, const double (&acc)[T::MI][T::NI][2]) {
     int b, s;
     decode(cur++, b, s);
     double* Cb = C + b * c_bs + s * split_stride;
-    tile::for_each_acc<CF>(t.m0, t.n0, t.o.M, t.o.N, acc,
-                           [&](int r, int c, double v) { Cb[(long long)r * c_rs + c] = v; });
+    tile::for_each_acc<T>(t.m0, t.n0, t.o.M, t.o.N, acc,
+                          [&](int r, int c, double v) { Cb[(long long)r * c_rs + c] = v; });
   };
-  tile::mma_stream<CF>(mine, get, epi, smem);
+  tile::mma_stream<T>(mine, get, epi, smem);
+}
+
+// Tile shapes selectable per phase (CGFusedArgs::tileA / tile3): the local ranks
+// (~96-112 at the C3 rank cap) make 64x64 tiles 60-80% full, so wider N tiles
+// that cover the whole rank in one tile are offered too.
+using T64x64 = CF;
+using T64x112 = tile::Cfg<64, 112, 16, 4, 2, 3>;  // warp tile 16x56
+using T32x112 = tile::Cfg<32, 112, 16, 4, 2, 3>;  // warp tile 8x56
+using T64x96 = tile::Cfg<64, 96, 16, 4, 2, 3>;    // warp tile 16x48
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t SMEM_MAX = cmax(cmax(T64x64::SMEM, T64x112::SMEM), cmax(T32x112::SMEM, T64x96::SMEM));
+
+template <class... Args>
+__device__ void phase_gemm_sel(int sel, Args... args) {
+  switch (sel) {
+    case 1: phase_gemm<T64x112>(args...); break;
+    case 2: phase_gemm<T32x112>(args...); break;
+    case 3: phase_gemm<T64x96>(args...); break;
+    default: phase_gemm<T64x64>(args...); break;
+  }
 }
 
 // q = A v  for the local operator, leaves q = sum of the split-K partials of step 3
@@ -122,29 +144,29 @@ __device__ __forceinline__ void phase_mark(const CGFusedArgs& a, int ph, unsigne
 __device__ void matvec_phases(const CGFusedArgs& a, const double* v, double* smem, cg::grid_group& grid,
                               unsigned long long& tp) {
   if (a.Bop != nullptr) {
-    // steps 1+2 composed: per X: t2[X][(m,b),V] = Bop[X][(m,b),(U,n)] @ v[(U,n),V]
-    tile::Operands oc{a.Bop, (long long)a.lk * a.n, 1, v, a.rk, 1, a.m * a.R1, a.rk, a.lk * a.n};
-    phase_gemm(oc, (long long)a.m * a.R1 * a.lk * a.n, 0, a.lb, a.t2, a.rk, (long long)a.m * a.R1 * a.rk, 1,
-               (oc.K + CF::BK - 1) / CF::BK, 0, smem);
+    // steps 1+2 composed, one GEMM over all X: t2[(X,m,b),V] = Bop[(X,m,b),(U,n)] @ v[(U,n),V]
+    tile::Operands oc{a.Bop, (long long)a.lk * a.n, 1, v, a.rk, 1, a.lb * a.m * a.R1, a.rk, a.lk * a.n};
+    phase_gemm_sel(a.tileA, oc, 0LL, 0LL, 1, a.t2, (long long)a.rk, 0LL, 1, (oc.K + 15) / 16, 0LL, smem);
     grid.sync();
     phase_mark(a, 1, tp);
   } else {
-  // step 1: t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
-  tile::Operands o1{a.phil, a.lk, 1, v, (long long)a.n * a.rk, 1, a.lb * a.lo, a.n * a.rk, a.lk};
-  phase_gemm(o1, 0, 0, 1, a.t1, (long long)a.n * a.rk, 0, 1, (o1.K + CF::BK - 1) / CF::BK, 0, smem);
-  grid.sync();
-  phase_mark(a, 0, tp);
-  // step 2: per X: t2[X][(m,b),V] = Ap[(m,b),(a,n)] @ t1[X][(a,n),V]
-  tile::Operands o2{a.Ap, (long long)a.lo * a.n, 1, a.t1, a.rk, 1, a.m * a.R1, a.rk, a.lo * a.n};
-  phase_gemm(o2, 0, (long long)a.lo * a.n * a.rk, a.lb, a.t2, a.rk, (long long)a.m * a.R1 * a.rk, 1,
-             (o2.K + CF::BK - 1) / CF::BK, 0, smem);
-  grid.sync();
-  phase_mark(a, 1, tp);
+    // step 1: t1[(X,a),(n,V)] = phil[(X,a),U] @ v[U,(n,V)]
+    tile::Operands o1{a.phil, a.lk, 1, v, (long long)a.n * a.rk, 1, a.lb * a.lo, a.n * a.rk, a.lk};
+    phase_gemm_sel(0, o1, 0LL, 0LL, 1, a.t1, (long long)a.n * a.rk, 0LL, 1, (o1.K + 15) / 16, 0LL, smem);
+    grid.sync();
+    phase_mark(a, 0, tp);
+    // step 2: per X: t2[X][(m,b),V] = Ap[(m,b),(a,n)] @ t1[X][(a,n),V]
+    tile::Operands o2{a.Ap, (long long)a.lo * a.n, 1, a.t1, a.rk, 1, a.m * a.R1, a.rk, a.lo * a.n};
+    phase_gemm_sel(a.tileA, o2, 0LL, (long long)a.lo * a.n * a.rk, a.lb, a.t2, (long long)a.rk,
+                   (long long)a.m * a.R1 * a.rk, 1, (o2.K + 15) / 16, 0LL, smem);
+    grid.sync();
+    phase_mark(a, 1, tp);
   }
   // step 3 (split-K): part3[s][(X,m),Y] = t2[(X,m),(b,V)] @ phir[Y,(b,V)]^T
   tile::Operands o3{a.t2, (long long)a.R1 * a.rk, 1, a.phir, 1, (long long)a.R1 * a.rk, a.lb * a.m, a.rb,
                     a.R1 * a.rk};
-  phase_gemm(o3, 0, 0, 1, a.part3, a.rb, 0, a.S3, a.kt_per3, (long long)a.lb * a.m * a.rb, smem);
+  phase_gemm_sel(a.tile3, o3, 0LL, 0LL, 1, a.part3, (long long)a.rb, 0LL, a.S3, a.kt_per3,
+                 (long long)a.lb * a.m * a.rb, smem);
   grid.sync();
   phase_mark(a, 2, tp);
 }
@@ -249,20 +271,36 @@ __global__ void __launch_bounds__(NT, 2) cg_fused_kernel(CGFusedArgs a) {
 int cg_fused_grid(int device) {
   static int cached = -1;
   if (cached > 0) return cached;
-  QTT_CUDA(cudaFuncSetAttribute(cg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+  QTT_CUDA(cudaFuncSetAttribute(cg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
   int per_sm = 0, sms = 0;
-  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, NT, CF::SMEM));
+  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, NT, SMEM_MAX));
   QTT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   cached = std::max(1, std::min(per_sm, 2)) * sms;
   return cached;
 }
 
-void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3) {
+int tile_bm(int sel) { return sel == 2 ? 32 : 64; }
+int tile_bn(int sel) { return sel == 1 || sel == 2 ? 112 : (sel == 3 ? 96 : 64); }
+
+// Tile shape for an N-wide phase: one tile spanning N when N is just above a
+// multiple of 64 (rank ~96-112), else 64x64.  QTT_CG_TILE_A / _3 force a shape.
+int pick_tile(int N, const char* env) {
+  if (const char* e = std::getenv(env)) return std::atoi(e);
+  if (N > 64 && N <= 96) return 3;
+  if (N > 96 && N <= 112) return 1;
+  return 0;
+}
+
+void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3, int& tileA,
+                   int& tile3) {
+  tileA = pick_tile(rk, "QTT_CG_TILE_A");
+  tile3 = pick_tile(rb, "QTT_CG_TILE_3");
   const int M3 = lb * m, N3 = rb, K3 = R1 * rk;
-  const int tiles = cdiv(M3, CF::BM) * cdiv(N3, CF::BN);
-  const int ktiles = cdiv(K3, CF::BK);
+  const int tiles = cdiv(M3, tile_bm(tile3)) * cdiv(N3, tile_bn(tile3));
+  const int ktiles = cdiv(K3, 16);
   // as many K slices as fit in one wave of the grid (no second round of tiles)
-  int want = std::max(1, std::min(grid / std::max(1, tiles), std::max(1, ktiles / 4)));
+  static const int cap = std::getenv("QTT_CG_S3CAP") ? std::atoi(std::getenv("QTT_CG_S3CAP")) : 1 << 20;
+  int want = std::max(1, std::min({grid / std::max(1, tiles), std::max(1, ktiles / 4), cap}));
   kt_per3 = cdiv(ktiles, want);
   S3 = cdiv(ktiles, kt_per3);
 }
@@ -287,7 +325,7 @@ void cg_fused_build_bop(const double* phil, int lb, int lo, int lk, const double
 
 void cg_fused_launch(const CGFusedArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
-  QTT_CUDA(cudaLaunchCooperativeKernel((void*)cg_fused_kernel, dim3(grid), dim3(NT), args, CF::SMEM, s));
+  QTT_CUDA(cudaLaunchCooperativeKernel((void*)cg_fused_kernel, dim3(grid), dim3(NT), args, SMEM_MAX, s));
   QTT_CHECK_LAUNCH();
 }
 

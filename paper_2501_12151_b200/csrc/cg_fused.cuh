@@ -26,6 +26,7 @@ struct CGFusedArgs {
   double* t2;     // lb*m*R1*rk
   double* part3;  // S3*dim split-K partials of step 3
   int S3, kt_per3;
+  int tileA, tile3;  // tile shape per phase (cg_fused_plan)
   double* red;  // 4*grid doubles (two partial-sum buffers)
   long long dim;
   double atol;
@@ -40,7 +41,8 @@ struct CGFusedArgs {
 };
 
 int cg_fused_grid(int device);
-void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3);
+void cg_fused_plan(int lb, int m, int rb, int R1, int rk, int grid, int& S3, int& kt_per3, int& tileA,
+                   int& tile3);
 // flops of one matvec with / without the composed left operator (host-side choice)
 double cg_fused_flops(int lb, int lo, int lk, int m, int n, int R1, int rb, int rk, bool composed);
 void cg_fused_build_bop(const double* phil, int lb, int lo, int lk, const double* Ap, int m, int n, int R1,
