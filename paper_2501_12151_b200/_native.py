@@ -13,7 +13,8 @@ import numpy as np
 
 from .errors import CapacityError, DeviceError, ShapeMismatchError, SolverError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt.so")
+# QTT_LIB overrides the library path (A/B timing of two builds on one GPU box)
+LIB_PATH = os.environ.get("QTT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt.so")
 
 _lib = None
 _lock = threading.Lock()

@@ -349,8 +349,7 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
       phir = phir_pad.p;
     }
     DBuf t2((long long)L.lb * L.m * K3p, c_.stream), part3((long long)pl.S3 * dim, c_.stream);
-    DBuf red(4LL * grid, c_.stream), skws((long long)grid * cg_tma_tile_doubles(), c_.stream);
-    DBuf flagsb(cdiv(grid, 2), c_.stream);
+    DBuf red(4LL * grid, c_.stream);
     CGTmaArgs a;
     std::memset(&a, 0, sizeof(a));
     make_tensor_map_2d(&a.map_bop, bop.p, (long long)L.lb * L.m * L.R1, rowsA, rowsA, pl.box1_a);
@@ -359,10 +358,13 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     make_tensor_map_2d(&a.map_phir, phir, L.rb, K3, K3p, pl.box2_a);
     make_tensor_map_2d(&a.map_t2, t2.p, (long long)L.lb * L.m, K3, K3p, pl.box2_b);
     a.lb = L.lb; a.m = L.m; a.R1 = L.R1; a.lk = L.lk; a.n = L.n; a.rb = L.rb; a.rk = L.rk; a.K3p = K3p;
-    a.cfg1 = pl.cfg1; a.cfg2 = pl.cfg2;
+    a.p1_rb = pl.p1_rb; a.p1_cb = pl.p1_cb; a.p2_rb = pl.p2_rb; a.p2_cb = pl.p2_cb;
+    a.p1_nf = pl.p1_nf; a.p1_dedupe = pl.p1_dedupe; a.p2_nf = pl.p2_nf; a.p2_dedupe = pl.p2_dedupe;
+    a.box1_a = pl.box1_a; a.box1_b = pl.box1_b; a.box2_a = pl.box2_a; a.box2_b = pl.box2_b;
+    a.stage_stride = pl.stage_stride;
+    a.stages = pl.stages;
     a.b = bT.p; a.invd = dT.p; a.x = xT.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
     a.t2 = t2.p; a.part3 = part3.p; a.S3 = pl.S3; a.kt_per3 = pl.kt_per3; a.red = red.p;
-    a.sk_ws = skws.p; a.sk_flags = (unsigned*)flagsb.p;
     a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;
     a.out_iters = c_.flags + 8;
     a.out_rnorm = c_.scal + 20;
@@ -372,16 +374,24 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     a.phase_ns = dbg ? (unsigned long long*)(c_.scal + 32) : nullptr;
     if (dbg) QTT_CUDA(cudaMemsetAsync(c_.scal + 32, 0, 6 * 8, c_.stream));
     static const bool dbg2 = std::getenv("QTT_DEBUG") && std::atoi(std::getenv("QTT_DEBUG")) >= 2;
-    DBuf ctans(dbg2 ? 3LL * grid : 1, c_.stream);
+    DBuf ctans(dbg2 ? 3LL * grid + 8 : 1, c_.stream);
     if (dbg2) {
-      QTT_CUDA(cudaMemsetAsync(ctans.p, 0, 24LL * grid, c_.stream));
+      QTT_CUDA(cudaMemsetAsync(ctans.p, 0, 24LL * grid + 64, c_.stream));
       a.cta_ns = (unsigned long long*)ctans.p;
     }
     cg_tma_launch(a, grid, c_.stream);
     if (dbg2) {
-      std::vector<unsigned long long> h(3 * grid);
-      QTT_CUDA(cudaMemcpyAsync(h.data(), ctans.p, 24LL * grid, cudaMemcpyDeviceToHost, c_.stream));
+      std::vector<unsigned long long> h(3 * grid + 8);
+      QTT_CUDA(cudaMemcpyAsync(h.data(), ctans.p, 24LL * grid + 64, cudaMemcpyDeviceToHost, c_.stream));
       c_.sync();
+      int itd = 0;
+      QTT_CUDA(cudaMemcpy(&itd, c_.flags + 8, 4, cudaMemcpyDeviceToHost));
+      const double nmv = itd + (xany ? 1 : 0);
+      std::fprintf(stderr, "[qtt] cg_tma CTA0 timeline us/matvec: p1 first-data %.2f loop-end %.2f epi-end %.2f "
+                   "stream-end %.2f | p2 first-data %.2f loop-end %.2f epi-end %.2f stream-end %.2f\n",
+                   h[3 * grid] / nmv / 1e3, h[3 * grid + 1] / nmv / 1e3, h[3 * grid + 2] / nmv / 1e3,
+                   h[3 * grid + 3] / nmv / 1e3, h[3 * grid + 4] / nmv / 1e3, h[3 * grid + 5] / nmv / 1e3,
+                   h[3 * grid + 6] / nmv / 1e3, h[3 * grid + 7] / nmv / 1e3);
       if (std::getenv("QTT_CTA_DUMP")) {
         std::fprintf(stderr, "[qtt] cta_dump");
         for (int i = 0; i < grid; ++i) std::fprintf(stderr, " %llu:%llu", h[2 * grid + i], h[i]);
@@ -412,7 +422,8 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
       c_.sync();
       std::fprintf(stderr, "[qtt] cg_fused dims %d,%d,%d R %d S3 %d tiles %d,%d composed %d grid %d iters %d: ns "
                    "step1 %llu step2 %llu step3 %llu red %llu upd %llu pupd %llu\n", L.lb, L.m, L.rb, L.R1, pl.S3,
-                   10 + pl.cfg1, 10 + pl.cfg2, 1, grid, it, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+                   100 * pl.p1_rb + pl.p1_cb, 100 * pl.p2_rb + pl.p2_cb, 1, grid, it, ph[0], ph[1], ph[2], ph[3],
+                   ph[4], ph[5]);
     }
     const int calls = it + (xany ? 1 : 0);
     c_.stats.cg_iters += it;

@@ -2,8 +2,8 @@
 // local matvec runs on the TMA tile engine (tma_tile.cuh).  Per iteration:
 //   phase 1  t2[(X,m,b),V] = sum_(U,n) Bop[(X,m,b),(U,n)] p^T[V,(U,n)]
 //            (Bop = left environment composed with the operator core, built once per
-//            solve; one GEMM over all X, balanced over the grid by stream-K: every CTA
-//            takes an equal run of k-tiles, split tiles are finished in a fixed order)
+//            solve; one GEMM over all X, every CTA an exact 1/148 share of the output,
+//            DMMA fragments dealt evenly to its warps -- tma_fb.cuh)
 //   phase 2  q^T[Y,(X,m)] = sum_(b,V) phir[Y,(b,V)] t2[(X,m),(b,V)]   (split-K)
 //   then the split-K reduction + p.q, the x/r/z update + r.r, r.z, and p = z + beta p,
 // phases separated by grid barriers, everything resident in L2/HBM between them.
@@ -11,23 +11,21 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "cg_tma.cuh"
-#include "tma_tile.cuh"
+#include "tma_fb.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace qtt {
 namespace {
 
-constexpr int NT = 256;
-using C64 = tma::Cfg<64, 64, 2, 4, 4>;       // warp tile 32x16
-using C64x112 = tma::Cfg<64, 112, 4, 2, 4>;  // warp tile 16x56
-using C112x64 = tma::Cfg<112, 64, 2, 4, 4>;  // warp tile 56x16
-constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-constexpr size_t SMEM = cmax(C64::SMEM, cmax(C64x112::SMEM, C112x64::SMEM));
-constexpr long long TILE_DOUBLES = 64 * 112;  // largest BM*BN (stream-K partial slot)
+constexpr int NT = 384;  // 12 warps (3 per scheduler), one CTA per SM
+constexpr int NW = NT / 32;
+static_assert(NW == tmafb::NWARP, "fragment dealing uses every warp");
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -35,22 +33,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// block-wide sums of two values, broadcast (red: >= 2*NW + 2 doubles of shared memory)
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   a = warp_sum(a);
   b = warp_sum(b);
   __syncthreads();
-  if (lane == 0) { red[warp] = a; red[8 + warp] = b; }
+  if (lane == 0) { red[warp] = a; red[NW + warp] = b; }
   __syncthreads();
   if (warp == 0) {
-    double x = lane < NT / 32 ? red[lane] : 0.0, y = lane < NT / 32 ? red[8 + lane] : 0.0;
+    double x = lane < NW ? red[lane] : 0.0, y = lane < NW ? red[NW + lane] : 0.0;
     x = warp_sum(x);
     y = warp_sum(y);
-    if (lane == 0) { red[16] = x; red[17] = y; }
+    if (lane == 0) { red[2 * NW] = x; red[2 * NW + 1] = y; }
   }
   __syncthreads();
-  a = red[16];
-  b = red[17];
+  a = red[2 * NW];
+  b = red[2 * NW + 1];
   __syncthreads();
 }
 
@@ -81,200 +80,171 @@ __device__ __forceinline__ void phase_mark(const CGTmaArgs& a, int ph, unsigned 
 // generic-proxy global writes -> later TMA (async-proxy) reads, across the grid barrier
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// Dispatch a region stream on the per-warp fragment count and A-row dedupe.
+template <class Get, class Epi>
+__device__ __forceinline__ void fb_stream(tmafb::Ring& ring, const tmafb::Boxes& bx, int nf, bool dedupe, int n,
+                                          Get get, Epi epi) {
+  if (dedupe) {
+    switch (nf) {
+      case 4: tmafb::stream<4, true>(ring, bx, n, get, epi); break;
+      case 6: tmafb::stream<6, true>(ring, bx, n, get, epi); break;
+      case 8: tmafb::stream<8, true>(ring, bx, n, get, epi); break;
+      case 10: tmafb::stream<10, true>(ring, bx, n, get, epi); break;
+      case 12: tmafb::stream<12, true>(ring, bx, n, get, epi); break;
+      default: tmafb::stream<16, true>(ring, bx, n, get, epi); break;
+    }
+  } else {
+    switch (nf) {
+      case 4: tmafb::stream<4, false>(ring, bx, n, get, epi); break;
+      case 6: tmafb::stream<6, false>(ring, bx, n, get, epi); break;
+      case 8: tmafb::stream<8, false>(ring, bx, n, get, epi); break;
+      case 10: tmafb::stream<10, false>(ring, bx, n, get, epi); break;
+      case 12: tmafb::stream<12, false>(ring, bx, n, get, epi); break;
+      default: tmafb::stream<16, false>(ring, bx, n, get, epi); break;
+    }
+  }
 }
 
-// ---- phase 1 (stream-K): t2 <- Bop . v^T
-template <class T>
-__device__ __noinline__ void phase1(const CGTmaArgs& a, const CUtensorMap* mv, tma::Ring& ring, unsigned epoch) {
+// ---- phase 1: t2 <- Bop . v^T.  CTA c owns fragment rows [c*FR/G, (c+1)*FR/G) in
+// row blocks of <= p1_rb fragments, times column blocks of <= p1_cb fragments.
+__device__ __noinline__ void phase1(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring& ring) {
   const int M = a.lb * a.m * a.R1, N = a.rk, K = a.lk * a.n;
-  const int tn = (N + T::BN - 1) / T::BN;
-  const int tm = (M + T::BM - 1) / T::BM;
+  const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int KT = (K + 15) / 16;
-  const long long U = (long long)tm * tn * KT;
   const int G = gridDim.x, c = blockIdx.x;
-  const long long u0 = U * c / G, u1 = U * (c + 1) / G;
-  if (u0 >= u1) return;
-  const int t_first = (int)(u0 / KT), t_last = (int)((u1 - 1) / KT);
-  const CUtensorMap* mb = &a.map_bop;
+  const int r0 = (int)((long long)c * FR / G), r1 = (int)((long long)(c + 1) * FR / G);
+  const int RB = a.p1_rb, CB = a.p1_cb;
+  const int nrb = (r1 - r0 + RB - 1) / RB, ncb = (FC + CB - 1) / CB;
+  const tmafb::Boxes bx{&a.map_bop, mv, a.box1_a, a.box1_b};
   auto get = [&](int i) {
-    tma::Item it;
-    it.ma = mb;
-    it.mb = mv;
-    const int t = t_first + i;
-    it.m0 = (t / tn) * T::BM;
-    it.n0 = (t % tn) * T::BN;
-    it.kb = (int)max(0LL, u0 - (long long)t * KT);
-    it.ke = (int)min((long long)KT, u1 - (long long)t * KT);
-    return it;
+    const int rb = i / ncb, cb = i - (i / ncb) * ncb;
+    tmafb::Region g;
+    g.m0 = (r0 + rb * RB) * 8;
+    g.mrows = min(RB, r1 - r0 - rb * RB) * 8;
+    g.n0 = cb * CB * 8;
+    g.ncols = min(CB, FC - cb * CB) * 8;
+    g.kb = 0;
+    g.ke = KT;
+    return g;
   };
   const int R1 = a.R1, rk = a.rk;
   const long long K3p = a.K3p;
   double* t2 = a.t2;
-  auto store = [&](const tma::Item& it, const double (&acc)[T::MI][T::NI][2]) {
-    tma::for_each<T>(it.m0, it.n0, M, N, acc, [&](int r, int col, double v) {
+  auto epi = [&](const tmafb::Region& g, const auto& fr, const auto& acc) {
+    tmafb::store(g, fr, acc, M, N, [&](int r) {
       const int xm = r / R1, bb = r - xm * R1;
-      t2[xm * K3p + (long long)bb * rk + col] = v;
+      return t2 + xm * K3p + (long long)bb * rk;
     });
   };
-  auto epi = [&](const tma::Item& it, const double (&acc)[T::MI][T::NI][2]) {
-    if (it.kb == 0 && it.ke == KT) {
-      store(it, acc);
-      return;
-    }
-    if (it.kb > 0) {  // contributor: publish the partial tile, fragment order (coalesced)
-      double* w = a.sk_ws + (long long)c * TILE_DOUBLES;
-      int e = 0;
-#pragma unroll
-      for (int i = 0; i < T::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < T::NI; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) w[(e++) * NT + threadIdx.x] = acc[i][j][h];
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) st_release(a.sk_flags + c, epoch);
-      return;
-    }
-    // finisher (owns k-tile 0): add the later CTAs' partials in CTA order (deterministic)
-    auto& sum = const_cast<double(&)[T::MI][T::NI][2]>(acc);  // the stream's own accumulator
-    const long long t = (long long)(it.m0 / T::BM) * tn + it.n0 / T::BN;
-    const long long tile_end = (t + 1) * KT;
-    for (int c2 = c + 1; c2 < G; ++c2) {
-      const long long s2 = U * c2 / G, e2 = U * (c2 + 1) / G;
-      if (s2 >= tile_end) break;
-      if (s2 >= e2) continue;
-      if (threadIdx.x == 0)
-        while (ld_acquire(a.sk_flags + c2) < epoch) {
-        }
-      __syncthreads();
-      const double* w = a.sk_ws + (long long)c2 * TILE_DOUBLES;
-      int e = 0;
-#pragma unroll
-      for (int i = 0; i < T::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < T::NI; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) sum[i][j][h] += __ldcg(w + (e++) * NT + threadIdx.x);
-    }
-    store(it, sum);
-  };
-  tma::stream<T>(ring, t_last - t_first + 1, get, epi);
+  fb_stream(ring, bx, a.p1_nf, a.p1_dedupe != 0, r1 > r0 ? nrb * ncb : 0, get, epi);
 }
 
-// ---- phase 2 (split-K): part3[s][Y][(X,m)] = phir[Y, slice s] . t2[(X,m), slice s]
-template <class T>
-__device__ __noinline__ void phase2(const CGTmaArgs& a, tma::Ring& ring) {
+// ---- phase 2 (split-K): part3[s][Y][(X,m)] = phir[Y, slice s] . t2[(X,m), slice s];
+// one region per CTA: fragment-block tile x K slice.
+__device__ __noinline__ void phase2(const CGTmaArgs& a, tmafb::Ring& ring) {
   const int M = a.rb, N = a.lb * a.m, K = a.R1 * a.rk;
-  const int tm = (M + T::BM - 1) / T::BM, tn = (N + T::BN - 1) / T::BN;
+  const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int KT = (K + 15) / 16;
   const int S = a.S3, ktp = a.kt_per3;
-  const int items = tm * tn * S;
-  const int mine = items > (int)blockIdx.x ? (items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int RB = a.p2_rb, CB = a.p2_cb;
+  const int ntc = (FC + CB - 1) / CB, ntr = (FR + RB - 1) / RB;
+  const int items = ntr * ntc * S;
+  const tmafb::Boxes bx{&a.map_phir, &a.map_t2, a.box2_a, a.box2_b};
+  const int it0 = blockIdx.x;
   auto get = [&](int i) {
-    const int it = blockIdx.x + i * gridDim.x;
+    const int it = it0 + i * gridDim.x;
     const int s = it % S, tile = it / S;
-    tma::Item r;
-    r.ma = &a.map_phir;
-    r.mb = &a.map_t2;
-    r.m0 = (tile / tn) * T::BM;
-    r.n0 = (tile % tn) * T::BN;
-    r.kb = s * ktp;
-    r.ke = min(KT, r.kb + ktp);
-    return r;
+    const int tr = tile / ntc, tc = tile - (tile / ntc) * ntc;
+    tmafb::Region g;
+    g.m0 = tr * RB * 8;
+    g.mrows = min(RB, FR - tr * RB) * 8;
+    g.n0 = tc * CB * 8;
+    g.ncols = min(CB, FC - tc * CB) * 8;
+    g.kb = s * ktp;
+    g.ke = min(KT, g.kb + ktp);
+    return g;
   };
   const long long dim = a.dim;
   double* part3 = a.part3;
-  auto epi = [&](const tma::Item& it, const double (&acc)[T::MI][T::NI][2]) {
-    double* P = part3 + (long long)(it.kb / ktp) * dim;
-    tma::for_each<T>(it.m0, it.n0, M, N, acc, [&](int r, int col, double v) { P[(long long)r * N + col] = v; });
+  auto epi = [&](const tmafb::Region& g, const auto& fr, const auto& acc) {
+    double* P = part3 + (long long)(g.kb / ktp) * dim;
+    tmafb::store(g, fr, acc, M, N, [&](int r) { return P + (long long)r * N; });
   };
-  tma::stream<T>(ring, mine, get, epi);
+  const int mine = items > it0 ? (items - 1 - it0) / (int)gridDim.x + 1 : 0;
+  fb_stream(ring, bx, a.p2_nf, a.p2_dedupe != 0, mine, get, epi);
 }
 
-__device__ void matvec(const CGTmaArgs& a, const CUtensorMap* mv, tma::Ring& ring, unsigned& epoch,
-                       cg::grid_group& grid, unsigned long long& tp) {
-  ++epoch;
+__device__ void matvec(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring& ring, cg::grid_group& grid,
+                       unsigned long long& tp) {
   const unsigned long long ts = a.cta_ns != nullptr ? gtimer() : 0;
-  if (a.cfg1 == 1)
-    phase1<C64x112>(a, mv, ring, epoch);
-  else
-    phase1<C64>(a, mv, ring, epoch);
+  ring.dbg_slot = 0;
+  phase1(a, mv, ring);
   if (a.cta_ns != nullptr && threadIdx.x == 0) a.cta_ns[blockIdx.x] += gtimer() - ts;
-  const unsigned long long ts2 = a.cta_ns != nullptr ? gtimer() : 0;
   fence_proxy_global();
   grid.sync();
   phase_mark(a, 1, tp);
-  if (a.cfg2 == 1)
-    phase2<C112x64>(a, ring);
-  else
-    phase2<C64>(a, ring);
+  const unsigned long long ts2 = a.cta_ns != nullptr ? gtimer() : 0;
+  ring.dbg_slot = 1;
+  phase2(a, ring);
   if (a.cta_ns != nullptr && threadIdx.x == 0) a.cta_ns[gridDim.x + blockIdx.x] += gtimer() - ts2;
   grid.sync();
   phase_mark(a, 2, tp);
 }
 
-// Split-K reduction of this CTA's slice [e0, e1): KS consecutive lanes (a power of
-// two) share one element and take its partials k = g, g+KS, ...; their sums are
-// combined by a fixed xor tree, so the result is deterministic.  f(e, q) is called
-// by the group's lane 0.
+// Split-K reduction of this CTA's slice [e0, e1), NT elements at a time: warp w
+// sums partials k = w, w+NW, ... for every element of the chunk with all loads in
+// flight together, then the NW warp sums are added in warp order through shared
+// memory (deterministic).  f(e, q) runs on the thread owning element e.
 template <class F>
-__device__ __forceinline__ void reduce_slice(const CGTmaArgs& a, long long e0, long long e1, F&& f) {
-  const int cnt = (int)(e1 - e0);
-  if (cnt <= 0) return;
+__device__ __forceinline__ void reduce_slice(const CGTmaArgs& a, long long e0, long long e1, double* sred, F&& f) {
+  constexpr int W = NW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.S3;
-  int KS = 1;
-  while (KS * 2 <= S && KS * 2 <= 32 && KS * 2 * cnt <= NT) KS *= 2;
-  const int g = threadIdx.x & (KS - 1);
   const long long dim = a.dim;
   const double* part = a.part3;
-  // every lane of a warp runs the same number of element rounds (shuffles below)
-  const int rounds = (cnt + NT / KS - 1) / (NT / KS);
-  for (int rd = 0; rd < rounds; ++rd) {
-    const int el = rd * (NT / KS) + (int)threadIdx.x / KS;
-    const long long e = e0 + el;
-    double s = 0.0;
-    if (el < cnt) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = g;
-      for (; k + 3 * KS < S; k += 4 * KS) {
-        s0 += __ldcg(part + k * dim + e);
-        s1 += __ldcg(part + (k + KS) * dim + e);
-        s2 += __ldcg(part + (k + 2 * KS) * dim + e);
-        s3 += __ldcg(part + (k + 3 * KS) * dim + e);
+  for (long long c0 = e0; c0 < e1; c0 += NT) {
+    const int cnt = (int)min((long long)NT, e1 - c0);
+    double acc[W];
+#pragma unroll
+    for (int ch = 0; ch < W; ++ch) acc[ch] = 0.0;
+    for (int k = warp; k < S; k += W) {
+      const double* pk = part + k * dim + c0;
+#pragma unroll
+      for (int ch = 0; ch < W; ++ch) {
+        const int el = ch * 32 + lane;
+        if (el < cnt) acc[ch] += __ldcg(pk + el);
       }
-      for (; k < S; k += KS) s0 += __ldcg(part + k * dim + e);
-      s = (s0 + s1) + (s2 + s3);
     }
-    for (int o = 1; o < KS; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (el < cnt && g == 0) f(e, s);
+#pragma unroll
+    for (int ch = 0; ch < W; ++ch) sred[warp * NT + ch * 32 + lane] = acc[ch];
+    __syncthreads();
+    if ((int)threadIdx.x < cnt) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) s += sred[w * NT + threadIdx.x];
+      f(c0 + threadIdx.x, s);
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(NT, 2) cg_tma_kernel(const __grid_constant__ CGTmaArgs a) {
+__global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ CGTmaArgs a) {
   extern __shared__ unsigned char smem_raw[];
-  __shared__ double red[24];
+  __shared__ double red[2 * NW + 4];
   cg::grid_group grid = cg::this_grid();
   const long long n = a.dim;
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   const long long e0 = blockIdx.x * per, e1 = min(n, e0 + per);
   unsigned long long mv_ns = 0, t0 = 0, tp = gtimer();
   const bool timer = (blockIdx.x == 0 && threadIdx.x == 0);
-  tma::Ring ring = tma::ring_init<4>(smem_raw);
+  tmafb::Ring ring = tmafb::ring_init(smem_raw, a.stage_stride, a.stages);
+  if (a.cta_ns != nullptr) ring.dbg = a.cta_ns + 3 * gridDim.x;  // timeline of CTA 0's streams
   if (threadIdx.x == 0) {
-    a.sk_flags[blockIdx.x] = 0u;
     tma::prefetch_map(&a.map_bop);
     tma::prefetch_map(&a.map_p);
     tma::prefetch_map(&a.map_phir);
     tma::prefetch_map(&a.map_t2);
   }
-  unsigned epoch = 0;
   if (a.cta_ns != nullptr && threadIdx.x == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -285,7 +255,7 @@ __global__ void __launch_bounds__(NT, 2) cg_tma_kernel(const __grid_constant__ C
   // ---- r = b - A x0 (only when x0 has a nonzero entry, as scipy's `x.any()`)
   if (a.xany) {
     if (timer) t0 = gtimer();
-    matvec(a, &a.map_x, ring, epoch, grid, tp);
+    matvec(a, &a.map_x, ring, grid, tp);
     if (timer) mv_ns += gtimer() - t0;
   }
   double rr = 0.0, rz = 0.0;
@@ -298,8 +268,9 @@ __global__ void __launch_bounds__(NT, 2) cg_tma_kernel(const __grid_constant__ C
     rr += ri * ri;
     rz += ri * zi;
   };
+  double* sred = reinterpret_cast<double*>(ring.base);  // ring is idle between GEMM phases
   if (a.xany)
-    reduce_slice(a, e0, e1, init_r);
+    reduce_slice(a, e0, e1, sred, init_r);
   else
     for (long long e = e0 + threadIdx.x; e < e1; e += NT) init_r(e, 0.0);
   fence_proxy_global();
@@ -313,9 +284,9 @@ __global__ void __launch_bounds__(NT, 2) cg_tma_kernel(const __grid_constant__ C
 
   while (!(rnorm < a.atol) && it < a.maxiter) {
     if (timer) t0 = gtimer();
-    matvec(a, &a.map_p, ring, epoch, grid, tp);
+    matvec(a, &a.map_p, ring, grid, tp);
     double pq = 0.0, dummy = 0.0;
-    reduce_slice(a, e0, e1, [&](long long e, double qi) {
+    reduce_slice(a, e0, e1, sred, [&](long long e, double qi) {
       a.q[e] = qi;
       pq += __ldcg(a.p + e) * qi;
     });
@@ -379,44 +350,101 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
 
 bool cg_tma_supported(int lk, int n) { return ((long long)lk * n) % 2 == 0; }
 
+// the ring also serves as scratch for the split-K reduction (NW x NT doubles)
+constexpr size_t SMEM_MAX = 224 * 1024;  // + static shared memory <= the 227 KB opt-in limit
+size_t cg_tma_smem(int stride, int nst) {
+  return std::max((size_t)nst * stride, (size_t)NW * NT * sizeof(double)) + tmafb::HEADER + 1024 + 4096;
+}
+int cg_tma_stages(int) { return tmafb::STAGES; }
+
 int cg_tma_grid(int device) {
   static int cached = -1;
   if (cached > 0) return cached;
-  QTT_CUDA(cudaFuncSetAttribute(cg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  const size_t smem = std::getenv("QTT_TMA_ATTR_KB") ? (size_t)std::atoi(std::getenv("QTT_TMA_ATTR_KB")) * 1024
+                                                     : SMEM_MAX;
+  QTT_CUDA(cudaFuncSetAttribute(cg_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, sms = 0;
-  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_tma_kernel, NT, SMEM));
+  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_tma_kernel, NT, smem));
   QTT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  static const int want = std::getenv("QTT_TMA_PER_SM") ? std::atoi(std::getenv("QTT_TMA_PER_SM")) : 1;
-  cached = std::max(1, std::min(per_sm, want)) * sms;
+  if (per_sm < 1) throw Error(QTT_ERR_CUDA, "cg_tma_kernel cannot be resident (registers/shared memory)");
+  cached = sms;
   return cached;
 }
 
-long long cg_tma_tile_doubles() { return TILE_DOUBLES; }
-
 CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int grid) {
+  CGTmaPlan p{};
+  constexpr int FMAX = tmafb::MAXF * tmafb::NWARP;  // fragments per region
+  // phase 1: M1 x N1, each CTA ~FR/G fragment rows
+  const long long M1 = (long long)lb * m * R1;
+  const int FR1 = (int)cdiv(M1, 8), FC1 = cdiv(rk, 8);
+  p.p1_rb = std::max(1, std::min(32, cdiv(FR1, grid)));
+  p.p1_cb = std::max(1, std::min({FC1, FMAX / p.p1_rb, 32, 52 - p.p1_rb}));
+  if (const char* e = std::getenv("QTT_TMA_P1")) std::sscanf(e, "%d,%d", &p.p1_rb, &p.p1_cb);
+  p.box1_a = p.p1_rb * 8;
+  p.box1_b = p.p1_cb * 8;
+  p.p1_nf = tmafb::nf_for(p.p1_rb * p.p1_cb);
+  // dedupe needs every column block (the last may be narrower) to hold a run in 2 rows
+  const int cb1_min = FC1 % p.p1_cb == 0 ? p.p1_cb : FC1 % p.p1_cb;
+  p.p1_dedupe = tmafb::dedupe_ok(p.p1_nf, cb1_min) ? 1 : 0;
+  // phase 2: split-K; choose the fragment-block tiling and split count that
+  // minimise per-CTA DMMAs plus the split-K partial traffic
+  const int FR3 = cdiv(rb, 8), FC3 = cdiv(lb * m, 8);
+  const int KT3 = cdiv(R1 * rk, 16);
+  double best = 1e300;
+  for (int tr = cdiv(FR3, 32); tr <= FR3; ++tr) {
+    const int RB = cdiv(FR3, tr);
+    for (int tc = 1; tc <= FC3; ++tc) {
+      const int CB = cdiv(FC3, tc);
+      if (RB * CB > FMAX || RB > 32 || CB > 32 || RB + CB > 52) continue;
+      const int T = cdiv(FR3, RB) * cdiv(FC3, CB);
+      if (T > grid) continue;
+      const int want = std::max(1, std::min(grid / T, std::max(1, KT3 / 2)));
+      const int ktp = cdiv(KT3, want);
+      const int S = cdiv(KT3, ktp);
+      // per-CTA time in DMMA-clock units: NF-quantized fragments x k-tiles x (4 k-steps x
+      // 3 warps x 16 clk), + ~2.5 us first-data latency, + the partial store/reload
+      // per k-tile: DMMA issue (NF x 4 k-steps x 3 warps x 16 clk) or the L2->SMEM
+      // operand stream ((RB + CB) x 8 rows x 128 B at ~24 B/clk per SM), whichever is longer
+      // (or the ~2 us TMA round trip spread over the ring depth)
+      const int nst = cg_tma_stages(cdiv((RB + CB) * 8 * 128, 1024) * 1024);
+      const double per_kt = std::max({(double)tmafb::nf_for(RB * CB) * 4.0 * 48.0, (RB + CB) * 8.0 * 128.0 / 24.0,
+                                      4000.0 / (nst - 1)});
+      const double dmma = per_kt * ktp;
+      const double traffic = (double)S * rb * lb * m * 8.0 * 2.0 / 4.0e12 * 1.965e9;  // write+read at ~4 TB/s
+      const double c = dmma + 5000.0 + traffic;
+      if (c < best * 0.999) {
+        best = c;
+        p.p2_rb = RB;
+        p.p2_cb = CB;
+        p.S3 = S;
+        p.kt_per3 = ktp;
+      }
+    }
+  }
+  if (const char* e = std::getenv("QTT_TMA_P2")) {  // "rb,cb,S": force the phase-2 tiling (tuning)
+    int S = 0;
+    if (std::sscanf(e, "%d,%d,%d", &p.p2_rb, &p.p2_cb, &S) == 3 && S > 0) {
+      p.kt_per3 = cdiv(KT3, S);
+      p.S3 = cdiv(KT3, p.kt_per3);
+    }
+  }
+  p.box2_a = p.p2_rb * 8;
+  p.box2_b = p.p2_cb * 8;
+  p.p2_nf = tmafb::nf_for(p.p2_rb * p.p2_cb);
+  const int cb2_min = FC3 % p.p2_cb == 0 ? p.p2_cb : FC3 % p.p2_cb;
+  p.p2_dedupe = tmafb::dedupe_ok(p.p2_nf, cb2_min) ? 1 : 0;
+  const int bytes = std::max(p.box1_a + p.box1_b, p.box2_a + p.box2_b) * 128;
+  p.stage_stride = cdiv(bytes, 1024) * 1024;
+  p.stages = cg_tma_stages(p.stage_stride);
   (void)lk;
   (void)n;
-  CGTmaPlan p{};
-  static const int f1 = std::getenv("QTT_TMA_CFG1") ? std::atoi(std::getenv("QTT_TMA_CFG1")) : -1;
-  static const int f2 = std::getenv("QTT_TMA_CFG2") ? std::atoi(std::getenv("QTT_TMA_CFG2")) : -1;
-  p.cfg1 = f1 >= 0 ? f1 : (rk > 64 ? 1 : 0);
-  p.cfg2 = f2 >= 0 ? f2 : (rb > 64 ? 1 : 0);
-  p.box1_a = 64;
-  p.box1_b = p.cfg1 == 1 ? 112 : 64;
-  p.box2_a = p.cfg2 == 1 ? 112 : 64;
-  p.box2_b = 64;
-  const int M3 = rb, N3 = lb * m, K3 = R1 * rk;
-  const int tiles = cdiv(M3, p.box2_a) * cdiv(N3, p.box2_b);
-  const int ktiles = cdiv(K3, 16);
-  int want = std::max(1, std::min(grid / std::max(1, tiles), std::max(1, ktiles / 4)));
-  p.kt_per3 = cdiv(ktiles, want);
-  p.S3 = cdiv(ktiles, p.kt_per3);
   return p;
 }
 
 void cg_tma_launch(const CGTmaArgs& a, int grid, cudaStream_t s) {
   void* args[] = {(void*)&a};
-  QTT_CUDA(cudaLaunchCooperativeKernel((void*)cg_tma_kernel, dim3(grid), dim3(NT), args, SMEM, s));
+  QTT_CUDA(cudaLaunchCooperativeKernel((void*)cg_tma_kernel, dim3(grid), dim3(NT), args,
+                                       cg_tma_smem(a.stage_stride, a.stages), s));
   QTT_CHECK_LAUNCH();
 }
 

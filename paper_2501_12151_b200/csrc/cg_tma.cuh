@@ -18,7 +18,11 @@ struct CGTmaArgs {
   CUtensorMap map_t2;    // phase 2 B: t2 [(X,m)][(b,V)], row stride K3p
   int lb, m, R1, lk, n, rb, rk;
   long long K3p;
-  int cfg1, cfg2;  // tile shapes (cg_tma_plan)
+  int p1_rb, p1_cb, p2_rb, p2_cb;  // fragment-block sizes of the phase regions (cg_tma_plan)
+  int p1_nf, p1_dedupe, p2_nf, p2_dedupe;
+  int box1_a, box1_b, box2_a, box2_b;
+  int stage_stride;  // ring bytes per stage
+  int stages;        // ring depth
   const double* b;     // rhs^T
   const double* invd;  // Jacobi inverse diagonal ^T
   double* x;           // in: x0^T, out: solution^T
@@ -27,8 +31,6 @@ struct CGTmaArgs {
   double* part3;  // S3 * dim split-K partials of phase 2
   int S3, kt_per3;
   double* red;          // 4 * grid
-  double* sk_ws;        // stream-K partial tiles: grid * cg_tma_tile_doubles()
-  unsigned* sk_flags;   // grid
   long long dim;
   double atol;
   int maxiter;
@@ -41,13 +43,14 @@ struct CGTmaArgs {
 };
 
 struct CGTmaPlan {
-  int cfg1, cfg2, S3, kt_per3;
+  int p1_rb, p1_cb, p2_rb, p2_cb, S3, kt_per3;
+  int p1_nf, p1_dedupe, p2_nf, p2_dedupe;
   int box1_a, box1_b, box2_a, box2_b;  // TMA box rows per operand
+  int stage_stride, stages;
 };
 
 bool cg_tma_supported(int lk, int n);
 int cg_tma_grid(int device);
-long long cg_tma_tile_doubles();
 CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int grid);
 void cg_tma_launch(const CGTmaArgs& a, int grid, cudaStream_t s);
 // out[(v*rows + i)] = in[i*cols + v]  (rows = lk*n, cols = rk): [U][n][V] <-> [V][U][n]

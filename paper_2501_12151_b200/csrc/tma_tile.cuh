@@ -34,6 +34,16 @@ struct Cfg {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// 8-byte shared-memory load at a 32-bit shared address.  The ring base is realigned
+// at run time through integer arithmetic, which loses the pointer's address space:
+// plain C++ loads through it compile to generic LD with 64-bit address math per
+// fragment (measured: half the DMMA rate); explicit ld.shared keeps LDS + 32-bit adds.
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -72,6 +82,18 @@ __device__ __forceinline__ void load_2d(void* dst, const CUtensorMap* map, int x
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
+}
+
+// Column (in doubles) of the 128B-swizzled 16-double row that lane (lr, lc) reads in
+// k-step s (0..3) of a k-tile.  The k order inside a k-tile is free (it is summed
+// over), so k-step s takes the two 16-byte chunks s and s+4: lanes lc = 0,1 read
+// chunk s, lanes 2,3 chunk s+4.  Rows lr and lr^4 then share physical chunks only
+// across half-warps, so every half-warp's 16 8-byte loads hit 32 distinct banks
+// (with k-steps over consecutive chunk pairs, rows lr and lr^1 collided: 2-way
+// conflicts on half of all fragment loads, tools/tile_bench.cu + ncu).
+__device__ __forceinline__ int swz_off(int s, int lr, int lc) {
+  const int chunk = (s + ((lc >> 1) << 2)) ^ lr;
+  return (chunk << 1) | (lc & 1);
 }
 
 // One unit of work: output tile (m0, n0) of A.B^T over k-tiles [kb, ke).
@@ -128,21 +150,20 @@ __device__ __forceinline__ void issue(Ring& r, unsigned slot, const Item& it, in
 template <class C>
 __device__ __forceinline__ void compute(const Ring& r, unsigned slot, double (&acc)[C::MI][C::NI][2]) {
   const int s = slot % C::STAGES;
-  const double* sA = reinterpret_cast<const double*>(r.base + (size_t)s * C::STAGE_BYTES);
-  const double* sB = reinterpret_cast<const double*>(r.base + (size_t)s * C::STAGE_BYTES + C::A_BYTES);
+  const unsigned sA = smem_u32(r.base) + s * C::STAGE_BYTES;
+  const unsigned sB = sA + C::A_BYTES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm0 = (warp % C::WARPS_M) * C::WTM;
   const int wn0 = (warp / C::WARPS_M) * C::WTN;
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
   for (int ks = 0; ks < 16; ks += 4) {
-    const int k = ks + lc;
-    const int off = ((((k >> 1) ^ lr) << 1) | (k & 1));  // swizzled column of (row%8 == lr, k)
+    const int off = swz_off(ks >> 2, lr, lc);  // swizzled column of (row%8 == lr, k)
     double af[C::MI], bf[C::NI];
 #pragma unroll
-    for (int i = 0; i < C::MI; ++i) af[i] = sA[(wm0 + i * 8 + lr) * 16 + off];
+    for (int i = 0; i < C::MI; ++i) af[i] = lds64(sA + ((wm0 + i * 8 + lr) * 16 + off) * 8);
 #pragma unroll
-    for (int j = 0; j < C::NI; ++j) bf[j] = sB[(wn0 + j * 8 + lr) * 16 + off];
+    for (int j = 0; j < C::NI; ++j) bf[j] = lds64(sB + ((wn0 + j * 8 + lr) * 16 + off) * 8);
 #pragma unroll
     for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -170,6 +191,7 @@ __device__ __forceinline__ void stream(Ring& r, int n_items, Get get, Epi epi) {
   const unsigned first = r.uses;
   unsigned produced = first;
   if (threadIdx.x == 0) {
+    fence_proxy_async();  // earlier generic-proxy use of the ring's shared memory
     P = get(0);
     pk = P.kb;
     for (int s = 0; s < S - 1 && pi < n_items; ++s) {
@@ -234,6 +256,33 @@ __device__ __forceinline__ void for_each(int m0, int n0, int M, int N, const dou
       for (int t = 0; t < 2; ++t)
         if (row < M && col + t < N) f(row, col + t, acc[i][j][t]);
     }
+}
+
+// Store the accumulator tile row by row: rowptr(row) gives the destination of
+// column 0 of that (in-range) row; one call per row and fragment.
+template <class C, class RowPtr>
+__device__ __forceinline__ void store_rows(int m0, int n0, int M, int N, const double (&acc)[C::MI][C::NI][2],
+                                          RowPtr&& rowptr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp % C::WARPS_M) * C::WTM;
+  const int wn0 = (warp / C::WARPS_M) * C::WTN;
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int row = m0 + wm0 + i * 8 + lr;
+    if (row >= M) continue;
+    double* dst = rowptr(row);
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) {
+      const int col = n0 + wn0 + j * 8 + lc * 2;
+      if (col + 1 < N) {
+        dst[col] = acc[i][j][0];
+        dst[col + 1] = acc[i][j][1];
+      } else if (col < N) {
+        dst[col] = acc[i][j][0];
+      }
+    }
+  }
 }
 
 }  // namespace tma

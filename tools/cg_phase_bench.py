@@ -39,7 +39,7 @@ def main():
     tmp.seek(0)
     rows = {}
     for line in tmp:
-        if ("per-CTA" in line or "cta_dump" in line) and os.environ.get("QTT_SHOW_CTA"):
+        if ("per-CTA" in line or "cta_dump" in line or "timeline" in line) and os.environ.get("QTT_SHOW_CTA"):
             print(line.strip())
         m = LINE.search(line)
         if m:
