@@ -38,14 +38,15 @@ __device__ double block_sum(double v, double* red) {
 // ------------------------------------------------------------------ Householder QR
 // One CTA.  W is the column-major m x n working copy (shared memory when it fits,
 // else global scratch).  tau has k entries.
-template <int NT>
-__global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView Ro, double* gws,
-                                                int use_smem) {
+// (SMEM is a template parameter so the compiler knows W is shared: a runtime choice
+// between sm and gws makes W a generic pointer and every access a generic LD/ST)
+template <int NT, bool SMEM>
+__global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView Ro, double* gws) {
   extern __shared__ double sm[];
   __shared__ double red[40];
   const int m = in.rows, n = in.cols, k = min(m, n);
-  double* W = use_smem ? sm : gws;
-  double* tau = use_smem ? sm + (long long)m * n : gws + (long long)m * n;
+  double* W = SMEM ? sm : gws;
+  double* tau = W + (long long)m * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
 
@@ -125,22 +126,75 @@ __global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView
 
 // ------------------------------------------------------------------ one-sided Jacobi
 // Orthogonalizes the columns of the column-major m x n matrix W (round-robin
-// parallel ordering, one warp per column pair), accumulating V (n x n).
+// parallel ordering), accumulating V (n x n).  GS lanes own one column pair: each
+// lane holds its KMAX-row slice of both columns in registers for the whole rotation
+// (one shared-memory read and write per element per round), and the rotation test
+// gamma^2 > tol^2 alpha beta needs no square roots.
 // Outputs (sorted by descending norm): U = W/sigma (m x n view), s, Vt (n x n view).
-template <int NT>
+template <int GS, int KMAX>
+__device__ __forceinline__ bool rotate_pair(double* wa, double* wb, int len, int gl, bool live, double tol2,
+                                            double& cs, double& sn) {
+  double x[KMAX], y[KMAX];
+  double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int i = gl + k * GS;
+    const bool ok = live && i < len;
+    x[k] = ok ? wa[i] : 0.0;
+    y[k] = ok ? wb[i] : 0.0;
+    al = fma(x[k], x[k], al);
+    be = fma(y[k], y[k], be);
+    ga = fma(x[k], y[k], ga);
+  }
+#pragma unroll
+  for (int o = GS / 2; o > 0; o >>= 1) {
+    al += __shfl_xor_sync(0xffffffffu, al, o);
+    be += __shfl_xor_sync(0xffffffffu, be, o);
+    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+  }
+  if (!live || ga == 0.0 || !(ga * ga > tol2 * al * be)) return false;
+  const double zeta = (be - al) / (2.0 * ga);
+  const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+  cs = 1.0 / sqrt(1.0 + t * t);
+  sn = cs * t;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int i = gl + k * GS;
+    if (i < len) {
+      wa[i] = cs * x[k] - sn * y[k];
+      wb[i] = sn * x[k] + cs * y[k];
+    }
+  }
+  return true;
+}
+
+template <int GS, int KMAX>
+__device__ __forceinline__ void rotate_v(double* va, double* vb, int len, int gl, double cs, double sn) {
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int i = gl + k * GS;
+    if (i < len) {
+      const double x = va[i], y = vb[i];
+      va[i] = cs * x - sn * y;
+      vb[i] = sn * x + cs * y;
+    }
+  }
+}
+
+template <int NT, int GS, int KMAX, bool SMEM>
 __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, double* so, MatView Vto,
-                                                    double* gws, int use_smem, double tol, int dbg) {
+                                                    double* gws, double tol, int dbg) {
   extern __shared__ double sm[];
   __shared__ int s_rot;
   int sweeps_done = 0;
   const int m = in.rows, n = in.cols;
-  double* W = use_smem ? sm : gws;                      // m x n, column-major
+  double* W = SMEM ? sm : gws;                          // m x n, column-major
   double* V = W + (long long)m * n;                     // n x n, column-major
   double* sig = V + (long long)n * n;                   // n
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
-  constexpr int GS = 8;  // lanes per column pair
-  const int gl = tid % GS;
+  const int gl = tid % GS, grp = tid / GS;
+  const double tol2 = tol * tol;
 
   for (long long e = tid; e < (long long)m * n; e += NT) {
     const int i = (int)(e % m), j = (int)(e / m);
@@ -153,53 +207,29 @@ __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, dou
   for (int sweep = 0; sweep < 80; ++sweep) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
+    int rotated = 0;
     for (int r = 0; r < P - 1; ++r) {
-      // GS lanes per column pair: all n/2 pairs of a round run concurrently
-      // warp-uniform trip count (the shuffles below need all 32 lanes)
-      for (int qb = warp * (32 / GS); qb < P / 2; qb += NT / GS) {
-        const int q = qb + lane / GS;
+      // every thread runs the same passes (the group shuffles need whole warps)
+      for (int base = 0; base < P / 2; base += NT / GS) {
+        const int q = base + grp;
         int a = 0, b = 0;
         if (q == 0) { a = r; b = P - 1; }
         else { a = (r + q) % (P - 1); b = (r - q + (P - 1)) % (P - 1); }
         const bool live = q < P / 2 && a < n && b < n;
         if (a > b) { const int t = a; a = b; b = t; }
-        double al = 0, be = 0, ga = 0;
-        double* wa = W + (long long)a * m;
-        double* wb = W + (long long)b * m;
-        if (live)
-          for (int i = gl; i < m; i += GS) {
-            const double x = wa[i], y = wb[i];
-            al += x * x; be += y * y; ga += x * y;
-          }
-#pragma unroll
-        for (int o = GS / 2; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        if (!live) { a = 0; b = 0; }
+        double cs = 1.0, sn = 0.0;
+        if (rotate_pair<GS, KMAX>(W + (long long)a * m, W + (long long)b * m, m, gl, live, tol2, cs, sn)) {
+          rotate_v<GS, KMAX>(V + (long long)a * n, V + (long long)b * n, n, gl, cs, sn);
+          rotated = 1;
         }
-        if (!live || ga == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = gl; i < m; i += GS) {
-          const double x = wa[i], y = wb[i];
-          wa[i] = cs * x - sn * y;
-          wb[i] = sn * x + cs * y;
-        }
-        double* va = V + (long long)a * n;
-        double* vb = V + (long long)b * n;
-        for (int i = gl; i < n; i += GS) {
-          const double x = va[i], y = vb[i];
-          va[i] = cs * x - sn * y;
-          vb[i] = sn * x + cs * y;
-        }
-        if (gl == 0) s_rot = 1;
       }
       __syncthreads();
     }
+    if (rotated) s_rot = 1;
+    __syncthreads();
     sweeps_done = sweep + 1;
     if (!s_rot) break;
-    __syncthreads();
   }
   if (dbg && tid == 0) printf("[qtt] jacobi %dx%d sweeps %d\n", m, n, sweeps_done);
   // column norms
@@ -487,15 +517,15 @@ void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
   if (need <= kSmemDoubles) {
     static bool attr = false;
     if (!attr) {
-      QTT_CUDA(cudaFuncSetAttribute(qr_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      QTT_CUDA(cudaFuncSetAttribute(qr_kernel<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kSmemDoubles * 8));
       attr = true;
     }
-    qr_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, Q, R, nullptr, 1);
+    qr_kernel<NT, true><<<1, NT, need * 8, c.stream>>>(in, Q, R, nullptr);
     QTT_CHECK_LAUNCH();
   } else {
     DBuf ws(need, c.stream);
-    qr_kernel<NT><<<1, NT, 0, c.stream>>>(in, Q, R, ws.p, 0);
+    qr_kernel<NT, false><<<1, NT, 0, c.stream>>>(in, Q, R, ws.p);
     QTT_CHECK_LAUNCH();
   }
 }
@@ -505,23 +535,118 @@ static int jacobi_dbg() {
   return on;
 }
 
-static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
+template <int GS, int KMAX>
+static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt, double tol) {
+  // few lanes per pair and few warps: the rotation arithmetic is issued once per warp,
+  // so a round costs ~(warps x instructions) -- 256 threads cover 64 pairs at GS = 4
+  constexpr int NT = 256;
   const int m = in.rows, n = in.cols;
   const long long need = (long long)m * n + (long long)n * n + n;
-  constexpr int NT = 1024;
-  const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
   if (need <= kSmemDoubles) {
+    auto kern = jacobi_kernel<NT, GS, KMAX, true>;
     static bool attr = false;
     if (!attr) {
-      QTT_CUDA(cudaFuncSetAttribute(jacobi_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kSmemDoubles * 8));
+      QTT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDoubles * 8));
       attr = true;
     }
-    jacobi_kernel<NT><<<1, NT, need * 8, c.stream>>>(in, U, s, Vt, nullptr, 1, tol, jacobi_dbg());
+    kern<<<1, NT, need * 8, c.stream>>>(in, U, s, Vt, nullptr, tol, jacobi_dbg());
     QTT_CHECK_LAUNCH();
   } else {
     DBuf ws(need, c.stream);
-    jacobi_kernel<NT><<<1, NT, 0, c.stream>>>(in, U, s, Vt, ws.p, 0, tol, jacobi_dbg());
+    jacobi_kernel<NT, GS, KMAX, false><<<1, NT, 0, c.stream>>>(in, U, s, Vt, ws.p, tol, jacobi_dbg());
+    QTT_CHECK_LAUNCH();
+  }
+}
+
+static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
+  const int m = in.rows, n = in.cols;
+  const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
+  const int len = std::max(m, n);  // rows of W (m) and of V (n) per lane slice
+  if (len <= 4 * 32)
+    jacobi_launch<4, 32>(c, in, U, s, Vt, tol);
+  else if (len <= 8 * 32)
+    jacobi_launch<8, 32>(c, in, U, s, Vt, tol);
+  else if (len <= 16 * 32)
+    jacobi_launch<16, 32>(c, in, U, s, Vt, tol);
+  else if (len <= 32 * 32)
+    jacobi_launch<32, 32>(c, in, U, s, Vt, tol);
+  else
+    throw Error(QTT_ERR_ARG, "svd: matrix dimension above 1024 not supported by the Jacobi kernel");
+}
+
+namespace {
+
+// perm = columns of A (m x n) by decreasing 2-norm (stable), one CTA
+__global__ void __launch_bounds__(256) sort_cols_kernel(CMatView A, int* perm) {
+  extern __shared__ double nrm[];
+  const int m = A.rows, n = A.cols;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < n; j += 8) {
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      const double v = A.p[(long long)i * A.rs + (long long)j * A.cs];
+      s2 += v * v;
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) nrm[j] = s2;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += 256) {
+    const double v = nrm[j];
+    int r = 0;
+    for (int d = 0; d < n; ++d) r += (nrm[d] > v) || (nrm[d] == v && d < j);
+    perm[r] = j;
+  }
+}
+
+__global__ void gather_cols_kernel(CMatView A, const int* perm, double* out) {  // out row-major m x n
+  const long long total = (long long)A.rows * A.cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / A.cols), j = (int)(e % A.cols);
+    out[e] = A.p[(long long)i * A.rs + (long long)perm[j] * A.cs];
+  }
+}
+
+// Vt[k][perm[j]] = UX[j][k]   (UX n x n row-major)
+__global__ void scatter_vt_kernel(const double* UX, const int* perm, int n, MatView Vt) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n), k = (int)(e % n);
+    Vt.p[(long long)k * Vt.rs + (long long)perm[j] * Vt.cs] = UX[e];
+  }
+}
+
+}  // namespace
+
+// SVD of a tall matrix (m >= n) by preconditioned one-sided Jacobi: columns sorted by
+// decreasing norm, A P = Q R, then Jacobi on X = R^T (rows graded by the sort), so
+// R = V_X S U_X^T and A = (Q V_X) S (P U_X)^T.  On graded truncation matrices this
+// takes ~10 sweeps where Jacobi on R took 15-30 (tools/svd_bench.py).
+static void svd_tall(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
+  const int m = in.rows, n = in.cols;
+  DBuf permb(cdiv(n, 2) + 1, c.stream), Ap((long long)m * n, c.stream);
+  int* perm = reinterpret_cast<int*>(permb.p);
+  sort_cols_kernel<<<1, 256, n * sizeof(double), c.stream>>>(in, perm);
+  QTT_CHECK_LAUNCH();
+  gather_cols_kernel<<<grid_for((long long)m * n), 256, 0, c.stream>>>(in, perm, Ap.p);
+  QTT_CHECK_LAUNCH();
+  DBuf Q((long long)m * n, c.stream), R((long long)n * n, c.stream), UX((long long)n * n, c.stream),
+      VX((long long)n * n, c.stream);
+  qr(c, crowmajor(Ap.p, m, n), rowmajor(Q.p, m, n), rowmajor(R.p, n, n));
+  // Jacobi on R^T: UX (n x n) and V_X written untransposed into VX (row-major [i][rank])
+  jacobi(c, ctrans(crowmajor(R.p, n, n)), rowmajor(UX.p, n, n), s, trans(rowmajor(VX.p, n, n)));
+  if (U.p) {  // U = Q V_X
+    GemmArgs g;
+    g.M = m; g.N = n; g.K = n;
+    gemm_set_A(g, Q.p, n, false);
+    gemm_set_B(g, VX.p, n, false);
+    g.C = U.p; g.c_rs = U.rs; g.c_cs = U.cs;
+    gemm(g, c.stream);
+  }
+  if (Vt.p) {
+    scatter_vt_kernel<<<grid_for((long long)n * n), 256, 0, c.stream>>>(UX.p, perm, n, Vt);
     QTT_CHECK_LAUNCH();
   }
 }
@@ -530,34 +655,10 @@ void svd(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   const int m = in.rows, n = in.cols;
   if (m <= 0 || n <= 0) return;
   c.stats.svd_calls++;
-  if (m >= n) {
-    // in = Q R;  R = U_R S V^T  (Jacobi on R)  =>  U = Q U_R
-    DBuf Q((long long)m * n, c.stream), R((long long)n * n, c.stream), UR((long long)n * n, c.stream);
-    qr(c, in, rowmajor(Q.p, m, n), rowmajor(R.p, n, n));
-    jacobi(c, crowmajor(R.p, n, n), rowmajor(UR.p, n, n), s, Vt);
-    if (U.p) {
-      GemmArgs g;
-      g.M = m; g.N = n; g.K = n;
-      gemm_set_A(g, Q.p, n, false);
-      gemm_set_B(g, UR.p, n, false);
-      g.C = U.p; g.c_rs = U.rs; g.c_cs = U.cs;
-      gemm(g, c.stream);
-    }
-  } else {
-    // in^T = Q R (n x m, Q n x m, R m x m);  R = U_R S V_R^T  =>  in = V_R S (Q U_R)^T
-    DBuf Q((long long)n * m, c.stream), R((long long)m * m, c.stream), UR((long long)m * m, c.stream);
-    qr(c, ctrans(in), rowmajor(Q.p, n, m), rowmajor(R.p, m, m));
-    // Jacobi writes U_R and V_R^T; in's U = V_R  ->  pass U transposed as the "Vt" output
-    jacobi(c, crowmajor(R.p, m, m), rowmajor(UR.p, m, m), s, trans(U));
-    if (Vt.p) {  // Vt (m x n) = (Q U_R)^T = U_R^T Q^T
-      GemmArgs g;
-      g.M = m; g.N = n; g.K = m;
-      gemm_set_A(g, UR.p, m, true);
-      gemm_set_B(g, Q.p, m, true);
-      g.C = Vt.p; g.c_rs = Vt.rs; g.c_cs = Vt.cs;
-      gemm(g, c.stream);
-    }
-  }
+  if (m >= n)
+    svd_tall(c, in, U, s, Vt);
+  else  // in^T = U' S V'^T  =>  in = V' S U'^T
+    svd_tall(c, ctrans(in), trans(Vt), s, trans(U));
 }
 
 void potrf_lower(Ctx& c, double* A, int dim, long long ld, int* info) {
