@@ -55,7 +55,14 @@ struct PanelArgs {
   int jb;     // panel width
   double* tau;
   double* red;  // gridDim * (NB + 1) doubles
+  unsigned long long* tl;  // optional (QTT_DEBUG=2): CTA 0 per-step ns accumulators [5]
 };
+
+__device__ __forceinline__ unsigned long long qr_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Factor W[j0:m, j0:j0+jb].  Rows j0..m-1 are split over the CTAs; per column two
 // grid barriers: one after the partial norms, one after the partial dot products.
@@ -184,6 +191,20 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
     P[e] = W[(long long)(a.j0 + c) * ld + r0 + i];
   }
   __syncthreads();
+  // thread layout for the per-column partial dot products / reductions: column cc
+  // (< NB) times KS = PNT/NB sub-ranges, combined through shared memory in fixed order
+  constexpr int KS = PNT / NB;
+  __shared__ double sred[KS][NB];
+  const int tcc = threadIdx.x % NB, tsub = threadIdx.x / NB;
+  const bool tl = a.tl != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tc = tl ? qr_clock() : 0;
+  auto mark = [&](int i) {
+    if (tl) {
+      const unsigned long long now = qr_clock();
+      a.tl[i] += now - tc;
+      tc = now;
+    }
+  };
   for (int j = 0; j < a.jb; ++j) {
     const int rj = a.j0 + j;
     double* v = P + j * nloc;  // local rows r0..r1
@@ -196,14 +217,22 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
       a.red[blockIdx.x * (NB + 2)] = part;
       a.red[blockIdx.x * (NB + 2) + NB + 1] = own_rj ? v[rj - r0] : 0.0;  // alpha
     }
+    mark(0);
     cg::this_grid().sync();
+    mark(1);
     double xn = 0.0, al = 0.0;
     for (int b = threadIdx.x; b < G; b += PNT) {
       xn += __ldcg(a.red + b * (NB + 2));
       al += __ldcg(a.red + b * (NB + 2) + NB + 1);
     }
-    const double xnorm2 = block_sum(xn, red);
-    const double alpha = block_sum(al, red);  // exactly one CTA contributed
+    // one two-value block reduction (exactly one CTA contributed alpha)
+    xn = warp_sum(xn);
+    al = warp_sum(al);
+    if (lane == 0) { red[warp] = xn; red[16 + warp] = al; }
+    __syncthreads();
+    double xnorm2 = 0.0, alpha = 0.0;
+#pragma unroll
+    for (int w = 0; w < PNT / 32; ++w) { xnorm2 += red[w]; alpha += red[16 + w]; }
     double t = 0.0, beta = alpha, scal = 1.0;
     if (xnorm2 > 0.0) {  // dlarfg
       beta = -copysign(hypot(alpha, sqrt(xnorm2)), alpha);
@@ -215,32 +244,188 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.tau[rj] = t;
     __syncthreads();
     const int nrem = a.jb - j - 1;
-    if (t != 0.0 && nrem > 0) {
-      for (int cc = warp; cc < nrem; cc += PNT / 32) {
-        const double* wc = P + (j + 1 + cc) * nloc;
-        double s = 0.0;
-        for (int i = ib + lane; i < nloc; i += 32) s += v[i] * wc[i];
-        s = warp_sum(s);
-        if (lane == 0) a.red[blockIdx.x * (NB + 2) + 1 + cc] = s + (own_rj ? wc[rj - r0] : 0.0);
+    if (t != 0.0 && nrem > 0) {  // local partial dots  v . w_c  (+ w_c[rj] for the unit head)
+      double s = 0.0;
+      if (tcc < nrem) {
+        const double* wc = P + (j + 1 + tcc) * nloc;
+        const int len = (nloc - ib + KS - 1) / KS;
+        const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
+        for (int i = i0; i < i1; ++i) s += v[i] * wc[i];
+      }
+      sred[tsub][tcc] = s;
+      __syncthreads();
+      if (threadIdx.x < nrem) {
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) d += sred[k][threadIdx.x];
+        const double* wc = P + (j + 1 + threadIdx.x) * nloc;
+        a.red[blockIdx.x * (NB + 2) + 1 + threadIdx.x] = d + (own_rj ? wc[rj - r0] : 0.0);
       }
     }
+    mark(2);
     cg::this_grid().sync();
+    mark(3);
     if (t != 0.0 && nrem > 0) {
-      {  // 4 threads per column, all partial loads in flight at once; fixed order
-        const int cc = threadIdx.x >> 2, sub = threadIdx.x & 3;
-        double s = 0.0;
-        if (cc < nrem)
-          for (int b = sub; b < G; b += 4) s += __ldcg(a.red + b * (NB + 2) + 1 + cc);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (sub == 0 && cc < nrem) sw[cc] = s * t;
+      {  // sum the G partials of each column: KS interleaved sub-ranges per column, all
+         // loads independent (one L2 round trip), combined in fixed order
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (tcc < nrem) {
+          const double* base = a.red + 1 + tcc;
+          int b = tsub;
+          for (; b + 3 * KS < G; b += 4 * KS) {
+            s0 += __ldcg(base + (long long)b * (NB + 2));
+            s1 += __ldcg(base + (long long)(b + KS) * (NB + 2));
+            s2 += __ldcg(base + (long long)(b + 2 * KS) * (NB + 2));
+            s3 += __ldcg(base + (long long)(b + 3 * KS) * (NB + 2));
+          }
+          for (; b < G; b += KS) s0 += __ldcg(base + (long long)b * (NB + 2));
+        }
+        __syncthreads();  // sred reuse
+        sred[tsub][tcc] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (threadIdx.x < nrem) {
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < KS; ++k) d += sred[k][threadIdx.x];
+          sw[threadIdx.x] = d * t;
+        }
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < nrem * nloc; e += PNT) {
-        const int cc = e / nloc, i = e % nloc;
-        double* wc = P + (j + 1 + cc) * nloc;
-        if (i >= ib) wc[i] -= sw[cc] * v[i];
-        else if (own_rj && i == rj - r0) wc[i] -= sw[cc];
+      if (tcc < nrem) {  // same (column, row-range) layout as the dots: no index division
+        double* wc = P + (j + 1 + tcc) * nloc;
+        const double w = sw[tcc];
+        const int len = (nloc - ib + KS - 1) / KS;
+        const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
+        for (int i = i0; i < i1; ++i) wc[i] -= w * v[i];
+        if (tsub == 0 && own_rj) wc[rj - r0] -= w;
+      }
+      __syncthreads();
+    }
+    mark(4);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.jb; j += PNT) {
+    const int rj = a.j0 + j;
+    if (rj >= r0 && rj < r1) P[j * nloc + (rj - r0)] = sbeta[j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
+    const int c = e / nloc, i = e % nloc;
+    W[(long long)(a.j0 + c) * ld + r0 + i] = P[e];
+  }
+}
+
+// Panel factorization inside ONE thread-block cluster (up to 16 CTAs on one GPC):
+// the per-column reductions go through distributed shared memory and the two
+// barriers per column are hardware cluster barriers, instead of L2 round trips and
+// grid-wide barriers of 148 CTAs (tools: QTT_DEBUG=2 panel timeline, ~9 us/column).
+// Each CTA keeps its row block of the panel (<= ~200 KB) in shared memory.
+__global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
+  extern __shared__ double P[];  // [jb][nloc] column-major
+  __shared__ double red[40];
+  __shared__ double part[2];     // this CTA's partial norm^2 and alpha of the current column
+  __shared__ double dots[NB];    // this CTA's partial dots of the current column
+  __shared__ double sw[NB];
+  __shared__ double sbeta[NB];
+  // (column, row-range) thread layout: CW = panel width rounded to 32/64, KS = PNT/CW
+  __shared__ double sred[PNT];
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int rows = a.m - a.j0;
+  const int chunk = (rows + G - 1) / G;
+  const int r0 = a.j0 + rank * chunk, r1 = min(a.m, r0 + chunk);
+  const int nloc = max(0, r1 - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int CW = a.jb <= 32 ? 32 : 64, KS = PNT / CW;
+  const int tcc = threadIdx.x % CW, tsub = threadIdx.x / CW;
+  double* W = a.W;
+  const long long ld = a.ld;
+  for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
+    const int c = e / nloc, i = e % nloc;
+    P[e] = W[(long long)(a.j0 + c) * ld + r0 + i];
+  }
+  __syncthreads();
+  for (int j = 0; j < a.jb; ++j) {
+    const int rj = a.j0 + j;
+    double* v = P + j * nloc;
+    const int ib = max(0, rj + 1 - r0);
+    double pn = 0.0;
+#pragma unroll 4
+    for (int i = ib + threadIdx.x; i < nloc; i += PNT) pn = fma(v[i], v[i], pn);
+    pn = block_sum(pn, red);
+    const bool own_rj = (rj >= r0 && rj < r1);
+    if (threadIdx.x == 0) {
+      part[0] = pn;
+      part[1] = own_rj ? v[rj - r0] : 0.0;
+    }
+    cl.sync();
+    // every CTA sums the G partials in rank order (identical result everywhere)
+    double xnorm2 = 0.0, alpha = 0.0;
+    if (warp == 0) {
+      double x = 0.0, y = 0.0;
+      if (lane < G) {
+        const double* rp = cl.map_shared_rank(part, lane);
+        x = rp[0];
+        y = rp[1];
+      }
+      x = warp_sum(x);
+      y = warp_sum(y);
+      if (lane == 0) { red[32] = x; red[33] = y; }
+    }
+    __syncthreads();
+    xnorm2 = red[32];
+    alpha = red[33];
+    double t = 0.0, beta = alpha, scal = 1.0;
+    if (xnorm2 > 0.0) {  // dlarfg
+      beta = -copysign(hypot(alpha, sqrt(xnorm2)), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      for (int i = ib + threadIdx.x; i < nloc; i += PNT) v[i] *= scal;
+    }
+    if (threadIdx.x == 0) sbeta[j] = beta;
+    if (rank == 0 && threadIdx.x == 0) a.tau[rj] = t;
+    __syncthreads();
+    const int nrem = a.jb - j - 1;
+    if (t != 0.0 && nrem > 0) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (tcc < nrem) {
+        const double* wc = P + (j + 1 + tcc) * nloc;
+        const int len = (nloc - ib + KS - 1) / KS;
+        const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
+        int i = i0;
+        for (; i + 3 < i1; i += 4) {
+          s0 = fma(v[i], wc[i], s0);
+          s1 = fma(v[i + 1], wc[i + 1], s1);
+          s2 = fma(v[i + 2], wc[i + 2], s2);
+          s3 = fma(v[i + 3], wc[i + 3], s3);
+        }
+        for (; i < i1; ++i) s0 = fma(v[i], wc[i], s0);
+      }
+      sred[tsub * CW + tcc] = (s0 + s1) + (s2 + s3);
+      __syncthreads();
+      if (threadIdx.x < nrem) {
+        double d = 0.0;
+        for (int k = 0; k < KS; ++k) d += sred[k * CW + threadIdx.x];
+        const double* wc = P + (j + 1 + threadIdx.x) * nloc;
+        dots[threadIdx.x] = d + (own_rj ? wc[rj - r0] : 0.0);
+      }
+    }
+    cl.sync();
+    if (t != 0.0 && nrem > 0) {
+      if (threadIdx.x < nrem) {
+        double d = 0.0;
+        for (int r = 0; r < G; ++r) d += cl.map_shared_rank(dots, r)[threadIdx.x];
+        sw[threadIdx.x] = d * t;
+      }
+      __syncthreads();
+      if (tcc < nrem) {
+        double* wc = P + (j + 1 + tcc) * nloc;
+        const double w = sw[tcc];
+        const int len = (nloc - ib + KS - 1) / KS;
+        const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
+#pragma unroll 4
+        for (int i = i0; i < i1; ++i) wc[i] = fma(-w, v[i], wc[i]);
+        if (tsub == 0 && own_rj) wc[rj - r0] -= w;
       }
       __syncthreads();
     }
@@ -255,6 +440,50 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
     const int c = e / nloc, i = e % nloc;
     W[(long long)(a.j0 + c) * ld + r0 + i] = P[e];
   }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+constexpr int CLUSTER_SMEM_DOUBLES = 25 * 1024;  // 200 KB of panel rows per CTA
+
+// Launch the cluster panel when the panel fits 16 CTAs' shared memory; false otherwise.
+bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s) {
+  static int ok = -1;
+  static const int disabled = std::getenv("QTT_PANEL_CLUSTER") && std::atoi(std::getenv("QTT_PANEL_CLUSTER")) == 0;
+  if (disabled) return false;
+  constexpr int CL = 16;
+  const int chunk = (mrows + CL - 1) / CL;
+  if ((long long)chunk * jb > CLUSTER_SMEM_DOUBLES) return false;
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess &&
+             cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CLUSTER_SMEM_DOUBLES * 8) == cudaSuccess
+         ? 1
+         : 0;
+    cudaGetLastError();
+  }
+  if (!ok) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(PNT);
+  cfg.dynamicSmemBytes = (size_t)chunk * jb * 8;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel, pa);
+  if (e != cudaSuccess) {  // e.g. 16-CTA clusters not schedulable at this size: fall back
+    cudaGetLastError();
+    if (std::getenv("QTT_DEBUG"))
+      std::fprintf(stderr, "[qtt] cluster panel %dx%d not launched: %s\n", mrows, jb, cudaGetErrorString(e));
+    return false;
+  }
+  QTT_CHECK_LAUNCH();
+  return true;
 }
 
 int panel_grid(int rows) {
@@ -305,89 +534,182 @@ struct QrTimer {
   }
 };
 
+// Two-level blocked Householder QR: 64-column panels (panel_smem_kernel) are applied
+// to the rest of their 256-column outer block one at a time, while the columns right
+// of the outer block get ONE compact-WY update per outer block (V_big: m x 256,
+// T_big assembled from the panel T's), so the large trailing matrix is streamed
+// through HBM a quarter as often and its GEMMs run with K = 256.
+namespace {
+constexpr int NB2 = 256;
+
+void apply_wy_left(Ctx& c, const double* V, int mrows, int jb, const double* T, long long ldt, double* C,
+                   long long ld, int n2, DBuf& Y1, DBuf& Y2, DBuf& Wsk) {
+  // C (mrows x n2, column-major ld) <- (I - V T V^T)^T C = C - V T^T (V^T C)
+  if (Y1.n < (long long)jb * n2) Y1.alloc((long long)jb * n2, c.stream);
+  if (Y2.n < (long long)jb * n2) Y2.alloc((long long)jb * n2, c.stream);
+  {  // Y1 = V^T C   (jb x n2)
+    GemmArgs g;
+    g.M = jb; g.N = n2; g.K = mrows;
+    g.A = V; g.a_rs = mrows; g.a_cs = 1;
+    g.B = C; g.b_rs = 1; g.b_cs = ld;
+    gemm_set_C(g, Y1.p, n2);
+    const long long need = gemm_workspace_hint(g);
+    if (Wsk.n < need) Wsk.alloc(need, c.stream);
+    gemm(g, c.stream, Wsk.p, Wsk.n);
+  }
+  {  // Y2 = T^T Y1
+    GemmArgs g;
+    g.M = jb; g.N = n2; g.K = jb;
+    g.A = T; g.a_rs = 1; g.a_cs = ldt;
+    gemm_set_B(g, Y1.p, n2, false);
+    gemm_set_C(g, Y2.p, n2);
+    gemm(g, c.stream);
+  }
+  {  // C -= V Y2
+    GemmArgs g;
+    g.M = mrows; g.N = n2; g.K = jb;
+    g.A = V; g.a_rs = 1; g.a_cs = mrows;
+    gemm_set_B(g, Y2.p, n2, false);
+    g.C = C; g.c_rs = 1; g.c_cs = ld;
+    g.alpha = -1.0; g.beta = 1.0;
+    gemm(g, c.stream);
+  }
+}
+
+void gram_vtv(Ctx& c, const double* V, int mrows, int jb, double* G, DBuf& Wsk) {  // G = V^T V (jb x jb)
+  GemmArgs g;
+  g.M = jb; g.N = jb; g.K = mrows;
+  g.A = V; g.a_rs = mrows; g.a_cs = 1;
+  g.B = V; g.b_rs = 1; g.b_cs = mrows;
+  gemm_set_C(g, G, jb);
+  const long long need = gemm_workspace_hint(g);
+  if (Wsk.n < need) Wsk.alloc(need, c.stream);
+  gemm(g, c.stream, Wsk.p, Wsk.n);
+}
+
+__global__ void copy_block_kernel(const double* src, int rows, int cols, long long lds, double* dst, long long ldd) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int i = e / cols, j = e % cols;
+    dst[i * ldd + j] = src[i * lds + j];
+  }
+}
+
+}  // namespace
+
 void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
   const int k = std::min(m, n);
   QrTimer tm(c.stream);
   tm.mark(0);
+  static const bool tl_on = std::getenv("QTT_DEBUG") && std::atoi(std::getenv("QTT_DEBUG")) >= 2;
+  DBuf tlbuf;
+  if (tl_on) {
+    tlbuf.alloc(8, c.stream);
+    QTT_CUDA(cudaMemsetAsync(tlbuf.p, 0, 64, c.stream));
+  }
   DBuf red(149LL * (NB + 2), c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
       T(NB * NB, c.stream), Y1, Y2, Wsk;
+  DBuf Vbig, Gbig, Tbig, P1;
   const long long ld = m;
-  for (int j0 = 0; j0 < k; j0 += NB) {
-    const int jb = std::min(NB, k - j0);
-    const int mrows = m - j0;
-    PanelArgs pa{W, ld, m, j0, jb, tau, red.p};
-    const int Gs = panel_smem_grid(mrows, jb);
-    if (Gs <= 148) {
-      static bool attr = false;
-      if (!attr) {
-        QTT_CUDA(cudaFuncSetAttribute(panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM_PANEL_DOUBLES * 8));
-        attr = true;
+  for (int J0 = 0; J0 < k; J0 += NB2) {
+    const int JB = std::min(NB2, k - J0);
+    const int jend = J0 + JB;  // columns right of this are updated once per outer block
+    const bool outer = n - jend > 0 && JB > NB / 2;
+    if (outer) {
+      Tbig.alloc((long long)JB * JB, c.stream);
+      QTT_CUDA(cudaMemsetAsync(Tbig.p, 0, (size_t)JB * JB * 8, c.stream));
+    }
+    // panel width: 64, or 32 when a 64-wide panel would not fit one 16-CTA cluster
+    static const int cl_rows = 16 * (CLUSTER_SMEM_DOUBLES / NB);
+    const int pw = (m - J0 > cl_rows) ? NB / 2 : NB;
+    for (int j0 = J0; j0 < jend; j0 += pw) {
+      const int jb = std::min(pw, jend - j0);
+      const int mrows = m - j0;
+      PanelArgs pa{W, ld, m, j0, jb, tau, red.p, tlbuf.p ? (unsigned long long*)tlbuf.p : nullptr};
+      const int Gs = panel_smem_grid(mrows, jb);
+      if (launch_panel_cluster(pa, mrows, jb, c.stream)) {
+      } else if (Gs <= 148) {
+        static bool attr = false;
+        if (!attr) {
+          QTT_CUDA(cudaFuncSetAttribute(panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SMEM_PANEL_DOUBLES * 8));
+          attr = true;
+        }
+        const int chunk = (mrows + Gs - 1) / Gs;
+        void* args[] = {(void*)&pa};
+        QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_smem_kernel, dim3(Gs), dim3(PNT), args,
+                                             (size_t)chunk * jb * 8, c.stream));
+      } else {
+        const int G = panel_grid(mrows);
+        void* args[] = {(void*)&pa};
+        QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PNT), args, 0, c.stream));
       }
-      const int chunk = (mrows + Gs - 1) / Gs;
-      void* args[] = {(void*)&pa};
-      QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_smem_kernel, dim3(Gs), dim3(PNT), args,
-                                           (size_t)chunk * jb * 8, c.stream));
-    } else {
-      const int G = panel_grid(mrows);
-      void* args[] = {(void*)&pa};
-      QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PNT), args, 0, c.stream));
+      QTT_CHECK_LAUNCH();
+      tm.mark(1);
+      // inner update: the rest of the outer block (or of the matrix when there is no outer step)
+      const int n2 = (outer ? jend : n) - j0 - jb;
+      const bool need_t = n2 > 0 || outer;
+      if (!need_t) continue;
+      build_v_kernel<<<std::min(1184, cdiv((long long)mrows * jb, 256)), 256, 0, c.stream>>>(W, ld, j0, mrows,
+                                                                                            jb, Vb.p);
+      QTT_CHECK_LAUNCH();
+      gram_vtv(c, Vb.p, mrows, jb, Gram.p, Wsk);
+      build_t_kernel<<<1, NB, 0, c.stream>>>(Gram.p, tau + j0, jb, T.p);
+      QTT_CHECK_LAUNCH();
+      if (outer) {  // keep the panel T as a diagonal block of T_big
+        copy_block_kernel<<<16, 256, 0, c.stream>>>(T.p, jb, jb, jb, Tbig.p + (long long)(j0 - J0) * JB + (j0 - J0),
+                                                    JB);
+        QTT_CHECK_LAUNCH();
+      }
+      tm.mark(2);
+      if (n2 > 0)
+        apply_wy_left(c, Vb.p, mrows, jb, T.p, jb, W + (long long)(j0 + jb) * ld + j0, ld, n2, Y1, Y2, Wsk);
+      tm.mark(5);
     }
+    if (!outer) continue;
+    // ---- one compact-WY update of the columns right of the outer block
+    const int mrowsJ = m - J0;
+    const int n2 = n - jend;
+    Vbig.alloc((long long)mrowsJ * JB, c.stream);
+    build_v_kernel<<<std::min(1184, cdiv((long long)mrowsJ * JB, 256)), 256, 0, c.stream>>>(W, ld, J0, mrowsJ, JB,
+                                                                                           Vbig.p);
     QTT_CHECK_LAUNCH();
-    tm.mark(1);
-    const int n2 = n - j0 - jb;
-    if (n2 <= 0) continue;
-    build_v_kernel<<<std::min(1184, cdiv((long long)mrows * jb, 256)), 256, 0, c.stream>>>(W, ld, j0, mrows,
-                                                                                          jb, Vb.p);
-    QTT_CHECK_LAUNCH();
-    {  // Gram = Vb^T Vb
-      GemmArgs g;
-      g.M = jb; g.N = jb; g.K = mrows;
-      g.A = Vb.p; g.a_rs = mrows; g.a_cs = 1;
-      g.B = Vb.p; g.b_rs = 1; g.b_cs = mrows;
-      gemm_set_C(g, Gram.p, jb);
-      const long long need = gemm_workspace_hint(g);  // one output tile, K = mrows: split K
-      if (Wsk.n < need) Wsk.alloc(need, c.stream);
-      gemm(g, c.stream, Wsk.p, Wsk.n);
+    Gbig.alloc((long long)JB * JB, c.stream);
+    gram_vtv(c, Vbig.p, mrowsJ, JB, Gbig.p, Wsk);
+    // T_big = [[T_1:k, -T_1:k (V_1:k^T V_k+1) T_k+1], [0, T_k+1]]  (dlarft block recursion)
+    P1.alloc((long long)JB * NB, c.stream);
+    for (int c0 = pw; c0 < JB; c0 += pw) {
+      const int w = std::min(pw, JB - c0);
+      {  // P1 (c0 x w) = T_big[0:c0, 0:c0] @ Gram[0:c0, c0:c0+w]
+        GemmArgs g;
+        g.M = c0; g.N = w; g.K = c0;
+        gemm_set_A(g, Tbig.p, JB, false);
+        gemm_set_B(g, Gbig.p + c0, JB, false);
+        gemm_set_C(g, P1.p, w);
+        gemm(g, c.stream);
+      }
+      {  // T_big[0:c0, c0:c0+w] = -P1 @ T_big[c0:c0+w, c0:c0+w]
+        GemmArgs g;
+        g.M = c0; g.N = w; g.K = w;
+        gemm_set_A(g, P1.p, w, false);
+        gemm_set_B(g, Tbig.p + (long long)c0 * JB + c0, JB, false);
+        gemm_set_C(g, Tbig.p + c0, JB);
+        g.alpha = -1.0;
+        gemm(g, c.stream);
+      }
     }
-    build_t_kernel<<<1, NB, 0, c.stream>>>(Gram.p, tau + j0, jb, T.p);
-    QTT_CHECK_LAUNCH();
     tm.mark(2);
-    if (Y1.n < (long long)jb * n2) Y1.alloc((long long)jb * n2, c.stream);
-    if (Y2.n < (long long)jb * n2) Y2.alloc((long long)jb * n2, c.stream);
-    double* C = W + (long long)(j0 + jb) * ld + j0;
-    {  // Y1 = Vb^T C   (jb x n2)
-      GemmArgs g;
-      g.M = jb; g.N = n2; g.K = mrows;
-      g.A = Vb.p; g.a_rs = mrows; g.a_cs = 1;
-      g.B = C; g.b_rs = 1; g.b_cs = ld;
-      gemm_set_C(g, Y1.p, n2);
-      const long long need = gemm_workspace_hint(g);
-      if (Wsk.n < need) Wsk.alloc(need, c.stream);
-      gemm(g, c.stream, Wsk.p, Wsk.n);
-    }
-    tm.mark(3);
-    {  // Y2 = T^T Y1
-      GemmArgs g;
-      g.M = jb; g.N = n2; g.K = jb;
-      g.A = T.p; g.a_rs = 1; g.a_cs = jb;
-      gemm_set_B(g, Y1.p, n2, false);
-      gemm_set_C(g, Y2.p, n2);
-      gemm(g, c.stream);
-    }
-    tm.mark(4);
-    {  // C -= Vb Y2
-      GemmArgs g;
-      g.M = mrows; g.N = n2; g.K = jb;
-      g.A = Vb.p; g.a_rs = 1; g.a_cs = mrows;
-      gemm_set_B(g, Y2.p, n2, false);
-      g.C = C; g.c_rs = 1; g.c_cs = ld;
-      g.alpha = -1.0; g.beta = 1.0;
-      gemm(g, c.stream);
-    }
+    apply_wy_left(c, Vbig.p, mrowsJ, JB, Tbig.p, JB, W + (long long)jend * ld + J0, ld, n2, Y1, Y2, Wsk);
     tm.mark(5);
   }
   tm.report(m, n);
+  if (tlbuf.p) {
+    unsigned long long h[5];
+    QTT_CUDA(cudaMemcpyAsync(h, tlbuf.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    QTT_CUDA(cudaStreamSynchronize(c.stream));
+    const double cols = std::max(1, std::min(m, n));
+    std::fprintf(stderr, "[qtt] geqrf %dx%d panel CTA0 ns/column: norm %.0f bar1 %.0f dlarfg+dots %.0f bar2 %.0f "
+                 "reduce+update %.0f\n", m, n, h[0] / cols, h[1] / cols, h[2] / cols, h[3] / cols, h[4] / cols);
+  }
 }
 
 }  // namespace qtt
