@@ -202,7 +202,7 @@ def run_reference(args, world, rank):
     info = None
     for _ in range(max(1, args.steps)):
         secs, info = cpu_baseline(trace, traj["certifications"], shapes, traj["sweeps"],
-                                  budget=max(5.0, min(25.0, 150.0 / max(1, args.steps))))
+                                  budget=max(10.0, min(25.0, 150.0 / max(1, args.steps))))
         times.append(secs)
     v = float(np.mean(times))
     line = {"metric": "time-to-solution at 2^30 cells (C3 QTT AMEn solve)", "value": v, "unit": "s",

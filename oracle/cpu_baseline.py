@@ -33,7 +33,7 @@ def host_cores() -> int:
     return os.cpu_count() or 1
 
 
-def _time(fn, min_time=0.05, max_reps=20):
+def _time_base(fn, min_time=0.05, max_reps=20):
     fn()  # warm
     reps, t0 = 0, time.perf_counter()
     while True:
@@ -76,11 +76,17 @@ class RateTable:
         return flops / self.rate(flops)
 
 
-def sample_rates(R=52, m=2, ranks=(8, 24, 48, 100), dense_dims=(256, 1024, 2304, 4096), seed=0,
-                 budget_s=25.0):
-    """Time the oracle primitives at representative shapes (the bounded sample)."""
+def sample_rates(R=52, m=2, ranks=(8, 16, 24, 32, 48, 64, 80, 100, 112),
+                 dense_dims=(256, 512, 1024, 2048, 2304, 3200, 4096), seed=0, budget_s=15.0):
+    """Time the oracle primitives at representative shapes (the bounded sample, about
+    budget_s of host work: every measurement repeats for ~budget_s / 60)."""
     rng = np.random.default_rng(seed)
     t_start = time.perf_counter()
+    mt = max(0.05, budget_s / 60.0)
+
+    def _time(fn, min_time=None, max_reps=200):
+        return _time_base(fn, min_time=mt if min_time is None else min_time, max_reps=max_reps)
+
     tables = {k: RateTable() for k in ("k1", "env", "dense", "chol", "svd", "qr")}
     shapes = []
     for r in ranks:
@@ -101,8 +107,8 @@ def sample_rates(R=52, m=2, ranks=(8, 24, 48, 100), dense_dims=(256, 1024, 2304,
     # one large unfolding, the size class of the certification sweeps
     big = rng.standard_normal((2048, 1024))
     tables["svd"].add(14.0 * 2048 * 1024 * 1024, _time(lambda: np.linalg.svd(big, full_matrices=False),
-                                                        max_reps=1))
-    tables["qr"].add(4.0 * 2048 * 1024 * 1024, _time(lambda: np.linalg.qr(big), max_reps=1))
+                                                        max_reps=3))
+    tables["qr"].add(4.0 * 2048 * 1024 * 1024, _time(lambda: np.linalg.qr(big), max_reps=3))
     for d in dense_dims:
         if time.perf_counter() - t_start > budget_s:
             break
@@ -111,7 +117,7 @@ def sample_rates(R=52, m=2, ranks=(8, 24, 48, 100), dense_dims=(256, 1024, 2304,
         phir = rng.standard_normal((rl, R, rl))
         A = rng.standard_normal((R, m, m, R))
         fl = 2.0 * rl * rl * R * m * m * R + 2.0 * (rl * m * rl) ** 2 * R
-        tables["dense"].add(fl, _time(lambda: O.local_dense(phil, A, phir), max_reps=3))
+        tables["dense"].add(fl, _time(lambda: O.local_dense(phil, A, phir), max_reps=10))
         g = rng.standard_normal((d, d))
         spd = g @ g.T + d * np.eye(d)
         b = rng.standard_normal(d)
@@ -121,7 +127,7 @@ def sample_rates(R=52, m=2, ranks=(8, 24, 48, 100), dense_dims=(256, 1024, 2304,
             scipy.linalg.cho_solve(c, b)
             float(np.abs(spd).sum(axis=1).max())
 
-        tables["chol"].add(d ** 3 / 3.0, _time(chol, max_reps=3))
+        tables["chol"].add(d ** 3 / 3.0, _time(chol, max_reps=10))
     return tables, {"ranks": shapes, "dense_dims": list(dense_dims),
                     "sample_s": time.perf_counter() - t_start}
 
