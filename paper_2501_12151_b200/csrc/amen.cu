@@ -353,7 +353,7 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     CGTmaArgs a;
     std::memset(&a, 0, sizeof(a));
     make_tensor_map_2d(&a.map_bop, bop.p, (long long)L.lb * L.m * L.R1, rowsA, rowsA, pl.box1_a);
-    make_tensor_map_2d(&a.map_p, p.p, L.rk, rowsA, rowsA, pl.box1_b);
+    make_tensor_map_2d(&a.map_z, z.p, L.rk, rowsA, rowsA, pl.box1_b);
     make_tensor_map_2d(&a.map_x, xT.p, L.rk, rowsA, rowsA, pl.box1_b);
     make_tensor_map_2d(&a.map_phir, phir, L.rb, K3, K3p, pl.box2_a);
     make_tensor_map_2d(&a.map_t2, t2.p, (long long)L.lb * L.m, K3, K3p, pl.box2_b);

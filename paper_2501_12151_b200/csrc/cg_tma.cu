@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
   if (a.cta_ns != nullptr) ring.dbg = a.cta_ns + 3 * gridDim.x;  // timeline of CTA 0's streams
   if (threadIdx.x == 0) {
     tma::prefetch_map(&a.map_bop);
-    tma::prefetch_map(&a.map_p);
+    tma::prefetch_map(&a.map_z);
     tma::prefetch_map(&a.map_phir);
     tma::prefetch_map(&a.map_t2);
   }
@@ -282,13 +282,32 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
   int it = 0;
   double* red_pq = a.red + 2 * gridDim.x;
 
+  // SciPy's recurrence with the search direction folded into the matvec: w = A z,
+  // then q = w + beta q (= A p since p = z + beta p) and p = z + beta p in the
+  // reduction phase -- one grid barrier per iteration less than q = A p after a
+  // separate p update.  (Identical in exact arithmetic; p = z, q = A z when beta = 0.)
+  double beta = 0.0;
   while (!(rnorm < a.atol) && it < a.maxiter) {
     if (timer) t0 = gtimer();
-    matvec(a, &a.map_p, ring, grid, tp);
+    matvec(a, &a.map_z, ring, grid, tp);
     double pq = 0.0, dummy = 0.0;
-    reduce_slice(a, e0, e1, sred, [&](long long e, double qi) {
+    const double bq = beta;
+    // this thread's element of a one-chunk slice: its q, z, p loads overlap the partial sums
+    const long long me = e0 + threadIdx.x;
+    const bool pre = (e1 - e0) <= NT && me < e1;
+    double q0 = 0.0, z0 = 0.0, p0 = 0.0;
+    if (pre) {
+      q0 = a.q[me];
+      z0 = a.z[me];
+      p0 = a.p[me];
+    }
+    reduce_slice(a, e0, e1, sred, [&](long long e, double wi) {
+      const bool hit = pre && e == me;
+      const double qi = wi + bq * (hit ? q0 : a.q[e]);
+      const double pi = (hit ? z0 : a.z[e]) + bq * (hit ? p0 : a.p[e]);
       a.q[e] = qi;
-      pq += __ldcg(a.p + e) * qi;
+      a.p[e] = pi;
+      pq += pi * qi;
     });
     block_sum2(pq, dummy, red);
     if (threadIdx.x == 0) { red_pq[2 * blockIdx.x] = pq; red_pq[2 * blockIdx.x + 1] = 0.0; }
@@ -300,8 +319,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
     rr = 0.0;
     rz = 0.0;
     for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
-      const double pi = __ldcg(a.p + e);
-      a.x[e] += alpha * pi;
+      a.x[e] += alpha * a.p[e];
       const double ri = a.r[e] - alpha * a.q[e];
       a.r[e] = ri;
       const double zi = ri * a.invd[e];
@@ -309,6 +327,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
       rr += ri * ri;
       rz += ri * zi;
     }
+    fence_proxy_global();  // z feeds the next matvec through TMA
     block_sum2(rr, rz, red);
     if (threadIdx.x == 0) { a.red[2 * blockIdx.x] = rr; a.red[2 * blockIdx.x + 1] = rz; }
     grid.sync();
@@ -317,12 +336,8 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
     ++it;
     rnorm = sqrt(rr);
     if (rnorm < a.atol || it >= a.maxiter) break;
-    const double beta = rz / rho;
+    beta = rz / rho;
     rho = rz;
-    for (long long e = e0 + threadIdx.x; e < e1; e += NT) a.p[e] = a.z[e] + beta * a.p[e];
-    fence_proxy_global();
-    grid.sync();
-    phase_mark(a, 5, tp);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *a.out_iters = it;

@@ -12,7 +12,7 @@ namespace qtt {
 // is what the TMA engine needs.
 struct CGTmaArgs {
   CUtensorMap map_bop;   // phase 1 A: Bop [(X,m,b)][(U,n)]
-  CUtensorMap map_p;     // phase 1 B: p^T [V][(U,n)]
+  CUtensorMap map_z;     // phase 1 B: z^T [V][(U,n)] (the CG matvec runs on z)
   CUtensorMap map_x;     // phase 1 B: x^T [V][(U,n)] (initial residual)
   CUtensorMap map_phir;  // phase 2 A: phir [Y][(b,V)], row stride K3p
   CUtensorMap map_t2;    // phase 2 B: t2 [(X,m)][(b,V)], row stride K3p
