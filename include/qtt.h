@@ -128,6 +128,15 @@ int qtt_tt_round(qtt_ctx* ctx, const qtt_train* a, double rel_tol, int max_rank,
                  qtt_train** out);                                            /* tt.py:409, 506 */
 int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x,
                  qtt_train** out);                                            /* tt.py:434 (policy=None) */
+/* Config-4 microbench: right-environment pre-pass (amen.py:300-321,
+ * _phi_right_step amen.py:114 with bra = ket = x), then one left-to-right sweep of
+ * _local_matvec(phi_L[k], A_k, phi_R[k+1], x_k) (amen.py:134) and
+ * _phi_left_step(phi_L[k], x_k, A_k, x_k) (amen.py:108).  y_out (optional) receives the
+ * local matvec outputs y_k (r_{k-1}, m_k, r_k) as a train.  times (optional, 7 doubles):
+ * pre-pass ms, sweep ms, K1 ms, K2 ms (split_timing != 0 only), K1 flops, K2 flops,
+ * pre-pass flops. */
+int qtt_matvec_sweep(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, int split_timing,
+                     qtt_train** y_out, double* times);
 /* ||Ax - f|| / ||f||.  method 0: the reference's QR-sweep norm of the difference train
  * (Kronecker-structured cores + blocked Householder QR); method 1: diagnostic Gram
  * estimate (fast, loses digits when ||A|| ||x|| >> ||Ax - f||). */

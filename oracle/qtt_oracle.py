@@ -253,6 +253,25 @@ def local_matvec(phil, a, phir, v):
     return np.tensordot(t, phir, axes=((3, 1), (1, 2)))   # X m Y
 
 
+def matvec_sweep(op, x):
+    """Config-4 microbench from the reference's own primitives: right
+    environments of x|A|x built right to left (amen.py:300-321 with _phi_right_step,
+    amen.py:114), then for k = 0..K-1 y_k = _local_matvec(phi_L[k], A_k, phi_R[k+1], x_k)
+    (amen.py:134) and phi_L[k+1] = _phi_left_step(phi_L[k], x_k, A_k, x_k) (amen.py:108)."""
+    K = len(op)
+    right = [None] * (K + 1)
+    right[K] = np.ones((1, 1, 1))
+    for k in range(K - 1, 0, -1):
+        right[k] = env_right(right[k + 1], x[k], op[k], x[k])
+    left = np.ones((1, 1, 1))
+    ys = []
+    for k in range(K):
+        ys.append(local_matvec(left, op[k], right[k + 1], x[k]))
+        if k + 1 < K:
+            left = env_left(left, x[k], op[k], x[k])
+    return ys
+
+
 def local_dense(phil, a, phir):
     """Dense local matrix, rows (X,m,Y), cols (U,n,V) (amen.py:140-144)."""
     t = np.tensordot(phil, a, axes=(1, 0))                # X U m n b

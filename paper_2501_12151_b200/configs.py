@@ -57,3 +57,14 @@ def build(w: Workload):
     x0 = x0_rank2(prob.dims, 0)
     kw = dict(residual_tol=w.tol, max_sweeps=w.max_sweeps, rounding=(w.tol, w.max_rank), seed=2024)
     return prob, x0, kw
+
+
+def c4_problem(r: int, d: int = 30, R: int = 16, seed: int = 1):
+    """Config 4 (BASELINE.json): rng = default_rng(seed); MPO cores
+    k = 0..d-1 of shape (1|R, 2, 2, R|1) first, then vector cores (1|r, 2, r|1), all
+    standard_normal * r**-0.5 (the literal reading of N(0, 1/r), MPO cores included)."""
+    rng = np.random.default_rng(seed)
+    s = r ** -0.5
+    op = [rng.standard_normal((1 if k == 0 else R, 2, 2, 1 if k == d - 1 else R)) * s for k in range(d)]
+    x = [rng.standard_normal((1 if k == 0 else r, 2, 1 if k == d - 1 else r)) * s for k in range(d)]
+    return op, x

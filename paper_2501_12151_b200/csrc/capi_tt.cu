@@ -7,6 +7,7 @@
 #include "amen.cuh"
 #include "contract.cuh"
 #include "linalg.cuh"
+#include "sweep.cuh"
 #include "capi_internal.cuh"
 
 namespace {
@@ -173,6 +174,26 @@ int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train
     qtt::Train y = qtt::tt_apply(c, ta, tx);
     c.sync();
     *out = wrap(std::move(y));
+  });
+}
+
+int qtt_matvec_sweep(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, int split_timing,
+                     qtt_train** y_out, double* times) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& tx = T(x);
+    T(A);
+    check_chain(tx);
+    qtt_train* Ah = const_cast<qtt_train*>(A);  // only the cached permuted views are added
+    qtt::SweepTimes st;
+    qtt::Train y = qtt::matvec_sweep(c, Ah->t, tx, times ? &st : nullptr, split_timing != 0);
+    c.sync();
+    if (times) {
+      const double v[7] = {st.prepass_ms, st.sweep_ms, st.k1_ms, st.k2_ms, st.k1_flops, st.k2_flops,
+                           st.prepass_flops};
+      for (int i = 0; i < 7; ++i) times[i] = v[i];
+    }
+    if (y_out) *y_out = wrap(std::move(y));
   });
 }
 

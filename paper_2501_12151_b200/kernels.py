@@ -143,3 +143,27 @@ def mixed_residual(psil, fc, psir, phil, ac, u, phir, ctx=None):
              nat.dptr(phil), nat.dptr(ac), nat.dptr(u), nat.dptr(phir),
              rX, rF, rG, rY, Ra, rU, m, n, Rb, rV, nat.dptr(out))
     return out
+
+
+SWEEP_TIME_FIELDS = ("prepass_ms", "sweep_ms", "k1_ms", "k2_ms", "k1_flops", "k2_flops", "prepass_flops")
+
+
+def matvec_sweep(A, x, ctx=None, timing=False, split_timing=False, return_y=True):
+    """Config-4 microbench operation: right-environment pre-pass, then one
+    left-to-right sweep of ``_local_matvec(phi_L[k], A_k, phi_R[k+1], x_k)`` (amen.py:134)
+    followed by ``_phi_left_step(phi_L[k], x_k, A_k, x_k)`` (amen.py:108), all on the device.
+
+    A / x: TTLinearOperator / TensorTrain (uploaded) or DeviceTrain handles (resident).
+    Returns (list of y_k cores or None, dict of CUDA-event times/flops or None)."""
+    import ctypes
+
+    from .tt import DeviceTrain
+    ctx = _ctx(ctx)
+    dA = A if isinstance(A, DeviceTrain) else DeviceTrain.upload(A.cores, ctx)
+    dx = x if isinstance(x, DeviceTrain) else DeviceTrain.upload(x.cores, ctx)
+    h = ctypes.c_void_p()
+    times = np.zeros(len(SWEEP_TIME_FIELDS))
+    nat.call("qtt_matvec_sweep", ctx.handle, dA.handle, dx.handle, 1 if split_timing else 0,
+             ctypes.byref(h) if return_y else None, nat.dptr(times) if timing else None)
+    ys = DeviceTrain(h, ctx).cores() if return_y else None
+    return ys, (dict(zip(SWEEP_TIME_FIELDS, times.tolist())) if timing else None)

@@ -266,7 +266,42 @@ def spd_op(dims, seed):
     return list(rtt.tt_op_add(rtt.tt_op_compose(rtt.tt_op_transpose(g), g), rtt.tt_identity(dims)).cores)
 
 
+def c4_cases():
+    """Config 4 at reduced size through the reference's own primitives: the matvec sweep
+    (right-env pre-pass, then _local_matvec + _phi_left_step per core) and
+    tt_round(tt_apply(A, x, None), TruncationPolicy(1e-8)) (tt.py:409, 434)."""
+    from paper_2501_12151_b200.configs import c4_problem
+    d = {}
+    for tag, (r, dd, R) in {"a": (6, 10, 4), "b": (16, 12, 16)}.items():
+        op, x = c4_problem(r, d=dd, R=R, seed=1)
+        K = len(op)
+        right = [None] * (K + 1)
+        right[K] = np.ones((1, 1, 1))
+        for k in range(K - 1, 0, -1):
+            right[k] = ram._phi_right_step(right[k + 1], x[k], op[k], x[k])
+        left = np.ones((1, 1, 1))
+        ys = []
+        for k in range(K):
+            ys.append(ram._local_matvec(left, op[k], right[k + 1], x[k]))
+            if k + 1 < K:
+                left = ram._phi_left_step(left, x[k], op[k], x[k])
+        put_train(d, f"{tag}_A", op)
+        put_train(d, f"{tag}_x", x)
+        put_train(d, f"{tag}_y", ys)
+        y = rtt.tt_apply(rtt.TTLinearOperator(op), rtt.TensorTrain(x), None)
+        yr = rtt.tt_round(y, rtt.TruncationPolicy(1e-8))
+        if tag == "a":  # (the rank-R*r product train is large; one small case is enough)
+            put_train(d, f"{tag}_apply", list(y.cores))
+        put_train(d, f"{tag}_round", list(yr.cores))
+        d[f"{tag}_round_norm"] = np.array(rtt.tt_norm(yr))
+    return d
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "c4":  # regenerate only the config-4 fixture
+        np.savez_compressed(os.path.join(HERE, "c4_small.npz"), **c4_cases())
+        return
+    np.savez_compressed(os.path.join(HERE, "c4_small.npz"), **c4_cases())
     np.savez_compressed(os.path.join(HERE, "kernels_bin.npz"), **kernels_case(1, (2,) * 8, 12, 6, 4))
     np.savez_compressed(os.path.join(HERE, "kernels_lead3.npz"), **kernels_case(2, (3,) + (2,) * 7, 10, 7, 4))
     np.savez_compressed(os.path.join(HERE, "factor.npz"), **factor_cases())
