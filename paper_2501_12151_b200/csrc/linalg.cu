@@ -6,6 +6,7 @@
 
 #include "gemm.cuh"
 #include "linalg.cuh"
+#include "svd_block.cuh"
 
 namespace qtt {
 namespace {
@@ -444,21 +445,37 @@ void reduce(Ctx& c, const double* a, const double* b, long long n, double* out) 
 }
 
 // ------------------------------------------------------------------ elementwise
-__global__ void kron_core_kernel(const double* A, int Ra0, int m, int n, int Ra1, const double* x,
-                                 int rx0, int rx1, double* y) {
-  const long long total = (long long)Ra0 * rx0 * m * Ra1 * rx1;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    long long t = e;
-    const int yy = (int)(t % rx1); t /= rx1;
-    const int b = (int)(t % Ra1); t /= Ra1;
-    const int mm = (int)(t % m); t /= m;
-    const int xx = (int)(t % rx0); t /= rx0;
-    const int a = (int)t;
-    double s = 0.0;
-    for (int nn = 0; nn < n; ++nn)
-      s += A[(((long long)a * m + mm) * n + nn) * Ra1 + b] * x[((long long)xx * n + nn) * rx1 + yy];
-    y[e] = s;
+// One CTA per output row (a, xx, mm): y[row, (b, yy)] = sum_n A[a,mm,n,b] x[xx,n,yy].  The
+// row's operator column A[a,mm,:,:] and vector slice x[xx,:,:] are staged in shared memory,
+// the row (Ra1 * rx1 doubles, contiguous) is written with coalesced streaming stores --
+// the kernel is a pure HBM write stream (tt.py:443-447).
+__global__ void __launch_bounds__(256) kron_core_kernel(const double* __restrict__ A, int Ra0, int m, int n,
+                                                        int Ra1, const double* __restrict__ x, int rx0, int rx1,
+                                                        double* __restrict__ y, int staged) {
+  extern __shared__ double sh[];
+  const long long rows = (long long)Ra0 * rx0 * m;
+  const int cols = Ra1 * rx1;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int mm = (int)(row % m);
+    const long long t = row / m;
+    const int xx = (int)(t % rx0), a = (int)(t / rx0);
+    const double* sa = A + ((long long)a * m + mm) * n * Ra1;  // A[a,mm,nn,b] at nn*Ra1 + b
+    const double* sx = x + (long long)xx * n * rx1;            // x[xx,nn,yy] at nn*rx1 + yy
+    if (staged) {  // (else: read through L1/L2 -- only for ranks beyond the shared-memory stage)
+      __syncthreads();
+      for (int i = threadIdx.x; i < n * Ra1; i += blockDim.x) sh[i] = sa[i];
+      for (int i = threadIdx.x; i < n * rx1; i += blockDim.x) sh[n * Ra1 + i] = sx[i];
+      __syncthreads();
+      sa = sh;
+      sx = sh + n * Ra1;
+    }
+    double* yr = y + row * cols;
+    for (int e = threadIdx.x; e < cols; e += blockDim.x) {
+      const int b = e / rx1, yy = e - b * rx1;
+      double s = 0.0;
+      for (int nn = 0; nn < n; ++nn) s += sa[nn * Ra1 + b] * sx[nn * rx1 + yy];
+      __stcs(yr + e, s);
+    }
   }
 }
 
@@ -514,6 +531,10 @@ void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
   const long long need = (long long)m * n + k;
   constexpr int NT = 512;
   c.stats.qr_calls++;
+  if (need > kSmemDoubles && k >= 64) {  // past one CTA's shared memory: blocked multi-CTA QR
+    qr_large(c, in, Q, R);
+    return;
+  }
   if (need <= kSmemDoubles) {
     static bool attr = false;
     if (!attr) {
@@ -560,6 +581,11 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
 
 static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   const int m = in.rows, n = in.cols;
+  static const int big_at = std::getenv("QTT_BJ_MIN") ? std::atoi(std::getenv("QTT_BJ_MIN")) : 256;
+  if (std::min(m, n) >= big_at) {
+    svd_block_jacobi(c, in, U, s, Vt);
+    return;
+  }
   const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
   const int len = std::max(m, n);  // rows of W (m) and of V (n) per lane slice
   if (len <= 4 * 32)
@@ -571,7 +597,7 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   else if (len <= 32 * 32)
     jacobi_launch<32, 32>(c, in, U, s, Vt, tol);
   else
-    throw Error(QTT_ERR_ARG, "svd: matrix dimension above 1024 not supported by the Jacobi kernel");
+    svd_block_jacobi(c, in, U, s, Vt);
 }
 
 namespace {
@@ -635,7 +661,7 @@ static void svd_tall(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   DBuf Q((long long)m * n, c.stream), R((long long)n * n, c.stream), UX((long long)n * n, c.stream),
       VX((long long)n * n, c.stream);
   qr(c, crowmajor(Ap.p, m, n), rowmajor(Q.p, m, n), rowmajor(R.p, n, n));
-  // Jacobi on R^T: UX (n x n) and V_X written untransposed into VX (row-major [i][rank])
+  // Jacobi on R^T (block one-sided Jacobi over all CTAs past one CTA's reach): UX (n x n) and V_X written untransposed into VX (row-major [i][rank])
   jacobi(c, ctrans(crowmajor(R.p, n, n)), rowmajor(UX.p, n, n), s, trans(rowmajor(VX.p, n, n)));
   if (U.p) {  // U = Q V_X
     GemmArgs g;
@@ -710,7 +736,12 @@ void read_scalars(Ctx& c, const double* dev, int n, double* host) {
 void kron_core(Ctx& c, const double* A, int Ra0, int m, int n, int Ra1, const double* x, int rx0,
                int rx1, double* y) {
   const long long total = (long long)Ra0 * rx0 * m * Ra1 * rx1;
-  kron_core_kernel<<<grid_for(total), 256, 0, c.stream>>>(A, Ra0, m, n, Ra1, x, rx0, rx1, y);
+  const long long rows = (long long)Ra0 * rx0 * m;
+  const size_t sh = (size_t)n * (Ra1 + rx1) * sizeof(double);
+  const int staged = sh <= 48 * 1024 ? 1 : 0;
+  (void)total;
+  kron_core_kernel<<<(int)std::min<long long>(rows, 148LL * 16), 256, staged ? sh : 0, c.stream>>>(
+      A, Ra0, m, n, Ra1, x, rx0, rx1, y, staged);
   QTT_CHECK_LAUNCH();
 }
 

@@ -543,8 +543,9 @@ namespace {
 constexpr int NB2 = 256;
 
 void apply_wy_left(Ctx& c, const double* V, int mrows, int jb, const double* T, long long ldt, double* C,
-                   long long ld, int n2, DBuf& Y1, DBuf& Y2, DBuf& Wsk) {
-  // C (mrows x n2, column-major ld) <- (I - V T V^T)^T C = C - V T^T (V^T C)
+                   long long ld, int n2, DBuf& Y1, DBuf& Y2, DBuf& Wsk, bool trans_t = true) {
+  // C (mrows x n2, column-major ld) <- (I - V T V^T)^T C = C - V T^T (V^T C)   (trans_t)
+  //                                 <- (I - V T V^T) C   = C - V T (V^T C)     (!trans_t, dorgqr)
   if (Y1.n < (long long)jb * n2) Y1.alloc((long long)jb * n2, c.stream);
   if (Y2.n < (long long)jb * n2) Y2.alloc((long long)jb * n2, c.stream);
   {  // Y1 = V^T C   (jb x n2)
@@ -560,7 +561,9 @@ void apply_wy_left(Ctx& c, const double* V, int mrows, int jb, const double* T, 
   {  // Y2 = T^T Y1
     GemmArgs g;
     g.M = jb; g.N = n2; g.K = jb;
-    g.A = T; g.a_rs = 1; g.a_cs = ldt;
+    g.A = T;
+    g.a_rs = trans_t ? 1 : ldt;
+    g.a_cs = trans_t ? ldt : 1;
     gemm_set_B(g, Y1.p, n2, false);
     gemm_set_C(g, Y2.p, n2);
     gemm(g, c.stream);
@@ -709,6 +712,34 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
     const double cols = std::max(1, std::min(m, n));
     std::fprintf(stderr, "[qtt] geqrf %dx%d panel CTA0 ns/column: norm %.0f bar1 %.0f dlarfg+dots %.0f bar2 %.0f "
                  "reduce+update %.0f\n", m, n, h[0] / cols, h[1] / cols, h[2] / cols, h[3] / cols, h[4] / cols);
+  }
+}
+
+namespace {
+__global__ void eye_kernel(double* Q, int m, int k) {  // column-major m x k identity
+  const long long total = (long long)m * k;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    Q[e] = (e % m) == (e / m) ? 1.0 : 0.0;
+}
+}  // namespace
+
+// dorgqr, blocked: Q = H_1 ... H_k I[:, :k], panels applied last to first, each as one
+// compact-WY product C <- (I - V T V^T) C on the trailing block Q[j0:, j0:].
+void orgqr_blocked(Ctx& c, const double* W, int m, int k, const double* tau, double* Q) {
+  eye_kernel<<<(int)std::min<long long>(cdiv((long long)m * k, 256), 1184), 256, 0, c.stream>>>(Q, m, k);
+  QTT_CHECK_LAUNCH();
+  DBuf Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream), T(NB * NB, c.stream), Y1, Y2, Wsk;
+  for (int j0 = ((k - 1) / NB) * NB; j0 >= 0; j0 -= NB) {
+    const int jb = std::min(NB, k - j0);
+    const int mrows = m - j0;
+    build_v_kernel<<<std::min(1184, cdiv((long long)mrows * jb, 256)), 256, 0, c.stream>>>(W, m, j0, mrows, jb,
+                                                                                          Vb.p);
+    QTT_CHECK_LAUNCH();
+    gram_vtv(c, Vb.p, mrows, jb, Gram.p, Wsk);
+    build_t_kernel<<<1, NB, 0, c.stream>>>(Gram.p, tau + j0, jb, T.p);
+    QTT_CHECK_LAUNCH();
+    apply_wy_left(c, Vb.p, mrows, jb, T.p, jb, Q + (long long)j0 * m + j0, m, k - j0, Y1, Y2, Wsk, false);
   }
 }
 

@@ -9,4 +9,8 @@ namespace qtt {
 // tau[min(m,n)] their scalars -- the LAPACK dgeqrf layout.
 void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau);
 
+// dorgqr: Q (m x k, column-major, leading dimension m) = the first k columns of
+// H_1 ... H_k from geqrf_blocked's reflectors (W, tau) -- LAPACK's Q, same signs.
+void orgqr_blocked(Ctx& c, const double* W, int m, int k, const double* tau, double* Q);
+
 }  // namespace qtt

@@ -1,6 +1,7 @@
 // TT algebra on device (tt.py): orthogonalization, norms, dots, rounding, apply,
 // and the residual norm of amen.py:87-99.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -204,8 +205,16 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
   bool all_one = true;
   for (int r : old) all_one = all_one && r == 1;
   if (K == 1 || all_one) return clone(c, a);
+  static const bool dbg = std::getenv("QTT_DEBUG") != nullptr;
+  auto now = [&]() {
+    if (dbg) c.sync();
+    return std::chrono::steady_clock::now();
+  };
+  const auto t0 = now();
   Train g = clone(c, a);
   orthogonalize_rl(c, g);
+  const auto t1 = now();
+  double t_svd = 0.0;
   nrm2(c, g.cores[0].d.p, g.cores[0].numel(), c.scal);
   const double nrm = read1(c, c.scal);
   if (nrm == 0.0) {
@@ -224,7 +233,9 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
     Core& ck = g.cores[k];
     const int rows = ck.r0 * ck.m * ck.n, cols = ck.r1, kk = std::min(rows, cols);
     DBuf U((long long)rows * kk, c.stream), s(kk, c.stream), Vt((long long)kk * cols, c.stream);
+    const auto ts0 = now();
     svd(c, crowmajor(ck.d.p, rows, cols), rowmajor(U.p, rows, kk), s.p, rowmajor(Vt.p, kk, cols));
+    t_svd += std::chrono::duration<double>(now() - ts0).count();
     hs.resize(kk);
     read_scalars(c, s.p, kk, hs.data());
     int r = rank_for_tolerance(hs.data(), kk, delta);
@@ -245,6 +256,10 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
     g.cores[k] = std::move(nk);
     g.cores[k + 1] = std::move(nn);
   }
+  if (dbg)
+    std::fprintf(stderr, "[qtt] tt_round K=%d: orthogonalize %.3f s, svd %.3f s, total %.3f s\n", K,
+                 std::chrono::duration<double>(t1 - t0).count(), t_svd,
+                 std::chrono::duration<double>(now() - t0).count());
   return g;
 }
 

@@ -93,3 +93,17 @@ def test_gpu_sweep_rejects_bad_shapes(K):
     op, x = c4_problem(4, d=5, R=3)
     with pytest.raises(ShapeMismatchError):
         K.matvec_sweep(tt.TTLinearOperator(op[:4]), tt.TensorTrain(x))
+
+
+@pytest.mark.gpu
+def test_gpu_round_config4_r32_vs_oracle():
+    """tt_round(tt_apply(A, x, None), 1e-8) at the config's r = 32 (bond 512, multi-CTA QR and
+    block-Jacobi SVD): ranks equal to the oracle's, difference <= 1e-12 relative (TT norm)."""
+    from paper_2501_12151_b200 import tt
+    from paper_2501_12151_b200.configs import c4_problem
+    op, x = c4_problem(32)
+    y = tt.tt_apply(tt.TTLinearOperator(op), tt.TensorTrain(x), tt.TruncationPolicy(1e-8))
+    ref = O.tt_round(O.tt_apply(op, x), 1e-8)
+    assert [c.shape for c in y.cores] == [c.shape for c in ref]
+    diff = O.tt_norm(O.tt_sub(list(y.cores), ref))
+    assert diff <= 1e-12 * O.tt_norm(ref)

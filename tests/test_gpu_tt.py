@@ -35,6 +35,42 @@ def test_qr_matches_numpy(tt, shape):
     assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-13 * k
 
 
+@pytest.mark.parametrize("shape", [(600, 300), (2100, 1030), (300, 900)])
+def test_qr_large_matches_numpy(tt, shape):
+    """Past one CTA's shared memory: blocked multi-CTA QR (geqrf + dorgqr), LAPACK signs."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    a = rng.standard_normal(shape)
+    q, r = tt._qr(a)
+    qn, rn = np.linalg.qr(a)
+    assert rel(q @ r, a) <= 1e-13
+    assert rel(q, qn) <= 1e-11 and rel(r, rn) <= 1e-12
+    k = min(shape)
+    assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-13 * k
+
+
+@pytest.mark.parametrize("shape,grade", [((700, 300), 10), ((1300, 1100), 12), ((520, 520), 0), ((300, 800), 6)])
+def test_svd_large_matches_numpy(tt, shape, grade):
+    """Block one-sided Jacobi (multi-CTA) on graded and flat spectra.  Like LAPACK gesdd
+    (tt.py:376-383) the factorization is backward stable: singular values to eps * s_max,
+    U s Vt to eps * ||a||, U orthonormal.  The rows of Vt come from normalized Jacobi columns,
+    so rows of singular values s << s_max are orthonormal only to ~eps * s_max / s: checked
+    on the rows with s >= 1e-3 s_max (the products S Vt used downstream are accurate)."""
+    rng = np.random.default_rng(shape[0] * 3 + shape[1])
+    a = rng.standard_normal(shape) * np.logspace(0, -grade, shape[1])[None, :]
+    u, s, vt = tt._svd(a)
+    sn = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(s - sn)) <= 1e-13 * sn[0]
+    assert rel(u @ np.diag(s) @ vt, a) <= 5e-13  # backward error ~ eps sqrt(n) x sweeps
+    k = min(shape)
+    big = int(np.sum(s >= 1e-3 * s[0]))
+    if shape[0] >= shape[1]:
+        assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-12 * k
+        assert np.linalg.norm(vt[:big] @ vt[:big].T - np.eye(big)) <= 1e-12 * k
+    else:  # wide: factored as the transpose, roles of U and Vt swap
+        assert np.linalg.norm(vt @ vt.T - np.eye(k)) <= 1e-12 * k
+        assert np.linalg.norm(u[:, :big].T @ u[:, :big] - np.eye(big)) <= 1e-12 * k
+
+
 def test_qr_rank_deficient(tt):
     rng = np.random.default_rng(3)
     a = rng.standard_normal((40, 5)) @ rng.standard_normal((5, 12))
