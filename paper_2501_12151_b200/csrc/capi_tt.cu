@@ -213,9 +213,9 @@ int qtt_qr(qtt_ctx* ctx, const double* mat, int rows, int cols, double* q, doubl
     if (rows < 1 || cols < 1) throw qtt::Error(QTT_ERR_SHAPE, "empty matrix");
     const int k = std::min(rows, cols);
     auto dm = up(mat, (long long)rows * cols, c.stream);
-    qtt::DBuf dq((long long)rows * k, c.stream), dr((long long)k * cols, c.stream);
-    qtt::qr(c, qtt::crowmajor(dm.p, rows, cols), qtt::rowmajor(dq.p, rows, k),
-            qtt::rowmajor(dr.p, k, cols));
+    qtt::DBuf dq(q ? (long long)rows * k : 0, c.stream), dr(r ? (long long)k * cols : 0, c.stream);
+    qtt::qr(c, qtt::crowmajor(dm.p, rows, cols), q ? qtt::rowmajor(dq.p, rows, k) : qtt::MatView{},
+            r ? qtt::rowmajor(dr.p, k, cols) : qtt::MatView{});
     if (q) dq.download(q, dq.n);
     if (r) dr.download(r, dr.n);
     c.sync();

@@ -56,6 +56,14 @@ struct PanelArgs {
   double* tau;
   double* red;  // gridDim * (NB + 1) doubles
   unsigned long long* tl;  // optional (QTT_DEBUG=2): CTA 0 per-step ns accumulators [5]
+  // cluster panel only (optional): write the unit lower trapezoid V (mrows x jb, column-
+  // major) and the block reflector T (jb x jb row-major upper; dlarft forward columnwise),
+  // also into T_big at (tb_off, tb_off) with leading dimension ldtb when Tb != nullptr
+  double* Vb = nullptr;
+  double* T = nullptr;
+  double* Tb = nullptr;
+  long long ldtb = 0;
+  int tb_off = 0;
 };
 
 __device__ __forceinline__ unsigned long long qr_clock() {
@@ -183,12 +191,13 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
   const int chunk = (rows + G - 1) / G;
   const int r0 = a.j0 + blockIdx.x * chunk, r1 = min(a.m, r0 + chunk);
   const int nloc = max(0, r1 - r0);
+  const int ldp = nloc | 1;  // odd column pitch: no bank conflicts across columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* W = a.W;
   const long long ld = a.ld;
   for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
     const int c = e / nloc, i = e % nloc;
-    P[e] = W[(long long)(a.j0 + c) * ld + r0 + i];
+    P[c * ldp + i] = W[(long long)(a.j0 + c) * ld + r0 + i];
   }
   __syncthreads();
   // thread layout for the per-column partial dot products / reductions: column cc
@@ -207,7 +216,7 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
   };
   for (int j = 0; j < a.jb; ++j) {
     const int rj = a.j0 + j;
-    double* v = P + j * nloc;  // local rows r0..r1
+    double* v = P + j * ldp;  // local rows r0..r1
     const int ib = max(0, rj + 1 - r0);  // first local row strictly below rj
     double part = 0.0;
     for (int i = ib + threadIdx.x; i < nloc; i += PNT) part += v[i] * v[i];
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
     if (t != 0.0 && nrem > 0) {  // local partial dots  v . w_c  (+ w_c[rj] for the unit head)
       double s = 0.0;
       if (tcc < nrem) {
-        const double* wc = P + (j + 1 + tcc) * nloc;
+        const double* wc = P + (j + 1 + tcc) * ldp;
         const int len = (nloc - ib + KS - 1) / KS;
         const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
         for (int i = i0; i < i1; ++i) s += v[i] * wc[i];
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
         double d = 0.0;
 #pragma unroll
         for (int k = 0; k < KS; ++k) d += sred[k][threadIdx.x];
-        const double* wc = P + (j + 1 + threadIdx.x) * nloc;
+        const double* wc = P + (j + 1 + threadIdx.x) * ldp;
         a.red[blockIdx.x * (NB + 2) + 1 + threadIdx.x] = d + (own_rj ? wc[rj - r0] : 0.0);
       }
     }
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
       }
       __syncthreads();
       if (tcc < nrem) {  // same (column, row-range) layout as the dots: no index division
-        double* wc = P + (j + 1 + tcc) * nloc;
+        double* wc = P + (j + 1 + tcc) * ldp;
         const double w = sw[tcc];
         const int len = (nloc - ib + KS - 1) / KS;
         const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
@@ -306,12 +315,12 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
   __syncthreads();
   for (int j = threadIdx.x; j < a.jb; j += PNT) {
     const int rj = a.j0 + j;
-    if (rj >= r0 && rj < r1) P[j * nloc + (rj - r0)] = sbeta[j];
+    if (rj >= r0 && rj < r1) P[j * ldp + (rj - r0)] = sbeta[j];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
     const int c = e / nloc, i = e % nloc;
-    W[(long long)(a.j0 + c) * ld + r0 + i] = P[e];
+    W[(long long)(a.j0 + c) * ld + r0 + i] = P[c * ldp + i];
   }
 }
 
@@ -323,7 +332,6 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
 __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
   extern __shared__ double P[];  // [jb][nloc] column-major
   __shared__ double red[40];
-  __shared__ double part[2];     // this CTA's partial norm^2 and alpha of the current column
   __shared__ double dots[NB];    // this CTA's partial dots of the current column
   __shared__ double sw[NB];
   __shared__ double sbeta[NB];
@@ -335,6 +343,9 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
   const int chunk = (rows + G - 1) / G;
   const int r0 = a.j0 + rank * chunk, r1 = min(a.m, r0 + chunk);
   const int nloc = max(0, r1 - r0);
+  // odd column pitch: lanes of a warp walk consecutive columns at the same row, so an even
+  // pitch would put all 32 of them in one shared-memory bank (32-way conflicts)
+  const int ldp = nloc | 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int CW = a.jb <= 32 ? 32 : 64, KS = PNT / CW;
   const int tcc = threadIdx.x % CW, tsub = threadIdx.x / CW;
@@ -342,31 +353,46 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
   const long long ld = a.ld;
   for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
     const int c = e / nloc, i = e % nloc;
-    P[e] = W[(long long)(a.j0 + c) * ld + r0 + i];
+    P[c * ldp + i] = W[(long long)(a.j0 + c) * ld + r0 + i];
   }
   __syncthreads();
+  const bool tl = a.tl != nullptr && rank == 0 && threadIdx.x == 0;
+  unsigned long long tc = tl ? qr_clock() : 0;
+  auto mark = [&](int i) {
+    if (tl) {
+      const unsigned long long now = qr_clock();
+      a.tl[i] += now - tc;
+      tc = now;
+    }
+  };
+  // inboxes: every CTA PUSHES its partials into all CTAs' shared memory before the cluster
+  // barrier (remote stores overlap the barrier), so the reductions after it read local smem
+  __shared__ double nin[16][2];
+  __shared__ double din[16][NB];
   for (int j = 0; j < a.jb; ++j) {
     const int rj = a.j0 + j;
-    double* v = P + j * nloc;
+    double* v = P + j * ldp;
     const int ib = max(0, rj + 1 - r0);
     double pn = 0.0;
 #pragma unroll 4
     for (int i = ib + threadIdx.x; i < nloc; i += PNT) pn = fma(v[i], v[i], pn);
     pn = block_sum(pn, red);
     const bool own_rj = (rj >= r0 && rj < r1);
-    if (threadIdx.x == 0) {
-      part[0] = pn;
-      part[1] = own_rj ? v[rj - r0] : 0.0;
+    if ((int)threadIdx.x < G) {
+      double* dst = cl.map_shared_rank(&nin[0][0], (int)threadIdx.x);
+      dst[2 * rank] = pn;
+      dst[2 * rank + 1] = own_rj ? v[rj - r0] : 0.0;
     }
+    mark(0);
     cl.sync();
-    // every CTA sums the G partials in rank order (identical result everywhere)
+    mark(1);
+    // every CTA sums the G partials in the same (lane-tree) order: identical result everywhere
     double xnorm2 = 0.0, alpha = 0.0;
     if (warp == 0) {
       double x = 0.0, y = 0.0;
       if (lane < G) {
-        const double* rp = cl.map_shared_rank(part, lane);
-        x = rp[0];
-        y = rp[1];
+        x = nin[lane][0];
+        y = nin[lane][1];
       }
       x = warp_sum(x);
       y = warp_sum(y);
@@ -389,7 +415,7 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
     if (t != 0.0 && nrem > 0) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (tcc < nrem) {
-        const double* wc = P + (j + 1 + tcc) * nloc;
+        const double* wc = P + (j + 1 + tcc) * ldp;
         const int len = (nloc - ib + KS - 1) / KS;
         const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
         int i = i0;
@@ -406,20 +432,28 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
       if (threadIdx.x < nrem) {
         double d = 0.0;
         for (int k = 0; k < KS; ++k) d += sred[k * CW + threadIdx.x];
-        const double* wc = P + (j + 1 + threadIdx.x) * nloc;
+        const double* wc = P + (j + 1 + threadIdx.x) * ldp;
         dots[threadIdx.x] = d + (own_rj ? wc[rj - r0] : 0.0);
       }
+      __syncthreads();
+      for (int e = threadIdx.x; e < G * nrem; e += PNT) {  // push to every CTA's inbox
+        const int r = e / nrem, cc = e - r * nrem;
+        cl.map_shared_rank(&din[0][0], r)[rank * NB + cc] = dots[cc];
+      }
     }
+    mark(2);
     cl.sync();
+    mark(3);
     if (t != 0.0 && nrem > 0) {
+      // sum each column's partials in rank order (same order in every CTA)
       if (threadIdx.x < nrem) {
         double d = 0.0;
-        for (int r = 0; r < G; ++r) d += cl.map_shared_rank(dots, r)[threadIdx.x];
+        for (int r = 0; r < G; ++r) d += din[r][threadIdx.x];
         sw[threadIdx.x] = d * t;
       }
       __syncthreads();
       if (tcc < nrem) {
-        double* wc = P + (j + 1 + tcc) * nloc;
+        double* wc = P + (j + 1 + tcc) * ldp;
         const double w = sw[tcc];
         const int len = (nloc - ib + KS - 1) / KS;
         const int i0 = ib + tsub * len, i1 = min(nloc, i0 + len);
@@ -429,18 +463,93 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
       }
       __syncthreads();
     }
+    mark(4);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < a.jb; j += PNT) {
     const int rj = a.j0 + j;
-    if (rj >= r0 && rj < r1) P[j * nloc + (rj - r0)] = sbeta[j];
+    if (rj >= r0 && rj < r1) P[j * ldp + (rj - r0)] = sbeta[j];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < nloc * a.jb; e += PNT) {
     const int c = e / nloc, i = e % nloc;
-    W[(long long)(a.j0 + c) * ld + r0 + i] = P[e];
+    W[(long long)(a.j0 + c) * ld + r0 + i] = P[c * ldp + i];
   }
-  cl.sync();  // no CTA leaves while another may still read its shared memory
+  if (a.T == nullptr) {
+    cl.sync();  // no CTA leaves while another may still read its shared memory
+    return;
+  }
+  // ---- V and T of the panel (replaces build_v + V^T V + dlarft launches)
+  __syncthreads();
+  const int mrows = a.m - a.j0, jb = a.jb;
+  for (int e = threadIdx.x; e < nloc * jb; e += PNT) {  // P -> V in place, and V out
+    const int c = e / nloc, i = e % nloc;
+    const int pr = r0 - a.j0 + i;  // row inside the panel
+    const double v = pr > c ? P[c * ldp + i] : (pr == c ? 1.0 : 0.0);
+    P[c * ldp + i] = v;
+    a.Vb[(long long)c * mrows + pr] = v;
+  }
+  __syncthreads();
+  // partial Gram of this CTA's rows: thread owns a 4x4 block of the 64x64 index space;
+  // Gp / Gs / Ts live in the (now free) dynamic panel buffer, sized for them at launch
+  double (*Gp)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(P);
+  double (*Gs)[NB + 1] = Gp + NB;
+  double (*Ts)[NB + 1] = Gp + 2 * NB;
+  {
+    const int p0 = 4 * (threadIdx.x >> 4), q0 = 4 * (threadIdx.x & 15);
+    double g[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) g[x][y] = 0.0;
+    if (p0 < jb && q0 < jb && q0 + 3 >= p0) {  // blocks touching the upper triangle
+      for (int i = 0; i < nloc; ++i) {
+        double vp[4], vq[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          vp[x] = p0 + x < jb ? P[(p0 + x) * ldp + i] : 0.0;
+          vq[x] = q0 + x < jb ? P[(q0 + x) * ldp + i] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) g[x][y] = fma(vp[x], vq[y], g[x][y]);
+      }
+    }
+    __syncthreads();  // every thread is done reading V from P
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) Gp[p0 + x][q0 + y] = g[x][y];
+  }
+  cl.sync();
+  if (rank == 0) {  // sum the partials in rank order, then the dlarft recursion in shared memory
+    for (int e = threadIdx.x; e < jb * jb; e += PNT) {
+      const int p = e / jb, q = e % jb;
+      double sum = 0.0;
+      if (p < q)
+        for (int r = 0; r < G; ++r) sum += cl.map_shared_rank(&Gp[0][0], r)[p * (NB + 1) + q];
+      Gs[p][q] = sum;
+      Ts[p][q] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < jb; ++j) {  // T[j][j] = tau_j;  T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
+      const double tj = a.tau[a.j0 + j];
+      if ((int)threadIdx.x < j) {
+        double acc = 0.0;
+        for (int q = threadIdx.x; q < j; ++q) acc = fma(Ts[threadIdx.x][q], Gs[q][j], acc);
+        Ts[threadIdx.x][j] = -tj * acc;
+      }
+      if (threadIdx.x == 0) Ts[j][j] = tj;
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < jb * jb; e += PNT) {
+      const int p = e / jb, q = e % jb;
+      a.T[e] = Ts[p][q];
+      if (a.Tb) a.Tb[(long long)(a.tb_off + p) * a.ldtb + a.tb_off + q] = Ts[p][q];
+    }
+  }
+  cl.sync();  // no CTA leaves while rank 0 may still read its shared memory
 }
 
 constexpr int CLUSTER_SMEM_DOUBLES = 25 * 1024;  // 200 KB of panel rows per CTA
@@ -452,7 +561,8 @@ bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s
   if (disabled) return false;
   constexpr int CL = 16;
   const int chunk = (mrows + CL - 1) / CL;
-  if ((long long)chunk * jb > CLUSTER_SMEM_DOUBLES) return false;
+  if ((long long)(chunk | 1) * jb > CLUSTER_SMEM_DOUBLES) return false;
+  const size_t dyn = std::max<size_t>((size_t)(chunk | 1) * jb, pa.T ? 3 * NB * (NB + 1) : 0) * 8;
   if (ok < 0) {
     ok = cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                  cudaSuccess &&
@@ -466,7 +576,7 @@ bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(PNT);
-  cfg.dynamicSmemBytes = (size_t)chunk * jb * 8;
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -496,7 +606,7 @@ int panel_grid(int rows) {
 // each CTA short: the panel is latency-bound, so more CTAs beat fuller ones.
 int panel_smem_grid(int rows, int jb) {
   static const int target = std::getenv("QTT_PANEL_ROWS") ? std::atoi(std::getenv("QTT_PANEL_ROWS")) : 64;
-  const int max_rows = SMEM_PANEL_DOUBLES / std::max(1, jb);
+  const int max_rows = SMEM_PANEL_DOUBLES / std::max(1, jb) - 1;  // (odd pitch: chunk | 1)
   const int need = std::max(1, (rows + max_rows - 1) / max_rows);
   const int want = std::min(148, std::max(1, (rows + target - 1) / std::max(1, target)));
   return std::max(need, want);
@@ -627,9 +737,20 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
     for (int j0 = J0; j0 < jend; j0 += pw) {
       const int jb = std::min(pw, jend - j0);
       const int mrows = m - j0;
+      const int n2 = (outer ? jend : n) - j0 - jb;
+      const bool need_t = n2 > 0 || outer;
       PanelArgs pa{W, ld, m, j0, jb, tau, red.p, tlbuf.p ? (unsigned long long*)tlbuf.p : nullptr};
+      if (need_t) {  // the cluster panel also emits V and T (and T's diagonal block of T_big)
+        pa.Vb = Vb.p;
+        pa.T = T.p;
+        pa.Tb = outer ? Tbig.p : nullptr;
+        pa.ldtb = JB;
+        pa.tb_off = j0 - J0;
+      }
       const int Gs = panel_smem_grid(mrows, jb);
+      bool have_vt = false;
       if (launch_panel_cluster(pa, mrows, jb, c.stream)) {
+        have_vt = need_t;
       } else if (Gs <= 148) {
         static bool attr = false;
         if (!attr) {
@@ -640,7 +761,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
         const int chunk = (mrows + Gs - 1) / Gs;
         void* args[] = {(void*)&pa};
         QTT_CUDA(cudaLaunchCooperativeKernel((void*)panel_smem_kernel, dim3(Gs), dim3(PNT), args,
-                                             (size_t)chunk * jb * 8, c.stream));
+                                             (size_t)(chunk | 1) * jb * 8, c.stream));
       } else {
         const int G = panel_grid(mrows);
         void* args[] = {(void*)&pa};
@@ -649,9 +770,8 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       QTT_CHECK_LAUNCH();
       tm.mark(1);
       // inner update: the rest of the outer block (or of the matrix when there is no outer step)
-      const int n2 = (outer ? jend : n) - j0 - jb;
-      const bool need_t = n2 > 0 || outer;
       if (!need_t) continue;
+      if (!have_vt) {
       build_v_kernel<<<std::min(1184, cdiv((long long)mrows * jb, 256)), 256, 0, c.stream>>>(W, ld, j0, mrows,
                                                                                             jb, Vb.p);
       QTT_CHECK_LAUNCH();
@@ -662,6 +782,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
         copy_block_kernel<<<16, 256, 0, c.stream>>>(T.p, jb, jb, jb, Tbig.p + (long long)(j0 - J0) * JB + (j0 - J0),
                                                     JB);
         QTT_CHECK_LAUNCH();
+      }
       }
       tm.mark(2);
       if (n2 > 0)

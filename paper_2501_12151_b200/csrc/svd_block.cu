@@ -296,6 +296,16 @@ __device__ bool pair_eig(double (*G)[2 * BS + 1], double (*Z)[2 * BS + 1], doubl
     if (!f) break;
     any = true;
   }
+  if (any) {  // renormalise Z's columns: hundreds of accumulated rotations would otherwise
+              // drift the column norms (and with them every singular value) by ~1e-13 per visit
+    if (t < P) {
+      double s2 = 0.0;
+      for (int i = 0; i < P; ++i) s2 = fma(Z[i][t], Z[i][t], s2);
+      const double inv = 1.0 / sqrt(s2);
+      for (int i = 0; i < P; ++i) Z[i][t] *= inv;
+    }
+    __syncthreads();
+  }
   return any;
 }
 
