@@ -1,6 +1,8 @@
 // FP64 DMMA GEMM (see gemm.cuh for the operand convention); the tile engine
 // itself lives in dmma_tile.cuh and is shared with the persistent fused kernels.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "dmma_tile.cuh"
 #include "gemm.cuh"
@@ -81,37 +83,52 @@ void launch(const GemmArgs& g, int splits, int kt_per, double* ws, cudaStream_t 
 using Cfg64 = tile::Cfg<64, 64, 16, 2, 2, 3>;
 using Cfg32 = tile::Cfg<32, 32, 16, 2, 2, 4>;
 using Cfg128 = tile::Cfg<128, 64, 16, 4, 2, 3>;
+using Cfg128x128 = tile::Cfg<128, 128, 16, 4, 2, 3>;
 
 constexpr int kSMs = 148;
 
 struct Plan {
-  int cfg;      // 0: 64x64, 1: 32x32, 2: 128x64
+  int cfg;      // 0: 64x64, 1: 32x32, 2: 128x64, 3: 128x128
   int splits;
   int kt_per;
 };
 
+// Pick the tile shape and split-K count with the smallest modelled time: full waves of
+// CTAs over the 148 SMs x (tile area x k-tiles) / relative per-SM DMMA efficiency of the
+// tile (bigger warp tiles issue fewer shared loads per DMMA and hide more latency), plus
+// the split-K partial traffic.  Split-K only for unbatched products short of a full wave.
 Plan plan_for(const GemmArgs& g) {
-  Plan p{0, 1, 0};
   const long long batch = (long long)g.batch1 * g.batch2;
-  if (g.M <= 40 || g.N <= 40)
-    p.cfg = 1;
-  else if (g.M >= 512 && (long long)cdiv(g.M, 128) * cdiv(g.N, 64) * batch >= 2 * kSMs)
-    p.cfg = 2;
-  const int bm = p.cfg == 1 ? 32 : (p.cfg == 2 ? 128 : 64);
-  const int bn = p.cfg == 1 ? 32 : 64;
-  const long long tiles = (long long)cdiv(g.M, bm) * cdiv(g.N, bn) * batch;
   const int ktiles = cdiv(g.K, 16);
-  p.kt_per = ktiles;
-  // Long-K products with too few output tiles to fill ~2 waves are split along K
-  // (fixed-order reduction), keeping >= 8 k-tiles per slice.
-  if (batch == 1 && tiles < 2 * kSMs && ktiles >= 16) {
-    int want = (int)std::min<long long>(cdiv(3 * kSMs, tiles), ktiles / 8);
-    if (want > 1) {
-      p.kt_per = cdiv(ktiles, want);
-      p.splits = cdiv(ktiles, p.kt_per);
+  struct Cand { int cfg, bm, bn; double eff; int per_sm; };
+  const Cand cands[] = {{3, 128, 128, 0.8, 1}, {2, 128, 64, 0.9, 2}, {0, 64, 64, 0.62, 3}, {1, 32, 32, 0.3, 4}};
+  Plan best{0, 1, ktiles};
+  double best_t = 1e300;
+  for (const Cand& c : cands) {
+    if (c.cfg == 3 && (g.M < 256 || g.N < 256)) continue;
+    if (c.cfg == 2 && g.M < 96) continue;
+    if (c.cfg != 1 && (g.M <= 40 || g.N <= 40)) continue;
+    const long long tiles = (long long)cdiv(g.M, c.bm) * cdiv(g.N, c.bn) * batch;
+    int splits = 1;
+    if (batch == 1 && tiles < (long long)kSMs * c.per_sm && ktiles >= 16) {
+      const int want = (int)std::min<long long>(std::max<long long>(1, (long long)kSMs * c.per_sm / tiles),
+                                                ktiles / 8);
+      splits = std::max(1, want);
+    }
+    const int kt_per = cdiv(ktiles, splits);
+    splits = cdiv(ktiles, kt_per);
+    const long long ctas = tiles * splits;
+    const double waves = std::ceil((double)ctas / ((double)kSMs * c.per_sm));
+    // time units: one DMMA-efficient 128x128x16 tile step = 1
+    double t = waves * c.per_sm * ((double)c.bm * c.bn / (128.0 * 128.0)) * kt_per / c.eff;
+    if (splits > 1) t += (double)splits * g.M * g.N * 16.0 / (128.0 * 128.0 * 16.0 * 2.0 * kSMs) * 4.0 + 2.0;
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best = Plan{c.cfg, splits, kt_per};
     }
   }
-  return p;
+  if (const char* e = std::getenv("QTT_GEMM_CFG")) best.cfg = std::atoi(e);  // tuning override
+  return best;
 }
 
 }  // namespace
@@ -146,6 +163,7 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
   switch (p.cfg) {
     case 1: launch<Cfg32>(g, p.splits, p.kt_per, ws, s); break;
     case 2: launch<Cfg128>(g, p.splits, p.kt_per, ws, s); break;
+    case 3: launch<Cfg128x128>(g, p.splits, p.kt_per, ws, s); break;
     default: launch<Cfg64>(g, p.splits, p.kt_per, ws, s); break;
   }
   if (p.splits > 1) {
