@@ -30,7 +30,7 @@ namespace qtt {
 namespace {
 
 constexpr int BJ_NT = 256;
-constexpr int BJ_CHUNK = 64;  // rows per staged tile
+constexpr int BJ_CHUNK = 256;  // rows per staged tile (double-buffered: ~64 KB in flight per SM)
 
 struct BJArgs {
   double* B;        // rows x ncols (column-major, ld = rows), ncols = nblk * BS (zero padded)
@@ -191,21 +191,33 @@ __device__ void pair_update(double* B, int brows, double* V, int vrows, int I, i
     }
     __syncthreads();
     double (*tile)[P + 1] = tiles[c & 1];
-    double acc[NC][2];
+    constexpr int RG = BJ_CHUNK / (8 * (BJ_NT / 32));  // 8-row groups per warp
+    double acc[RG][NC][2];
 #pragma unroll
-    for (int cb = 0; cb < NC; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+    for (int g = 0; g < RG; ++g)
+#pragma unroll
+      for (int cb = 0; cb < NC; ++cb) acc[g][cb][0] = acc[g][cb][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < P / 4; ++ks) {
-      const double a = tile[w * 8 + lr][ks * 4 + lc];
+      double zf[NC];
 #pragma unroll
-      for (int cb = 0; cb < NC; ++cb) dmma(acc[cb], a, Z[ks * 4 + lc][cb * 8 + lr]);
+      for (int cb = 0; cb < NC; ++cb) zf[cb] = Z[ks * 4 + lc][cb * 8 + lr];
+#pragma unroll
+      for (int g = 0; g < RG; ++g) {
+        const double a = tile[(g * (BJ_NT / 32) + w) * 8 + lr][ks * 4 + lc];
+#pragma unroll
+        for (int cb = 0; cb < NC; ++cb) dmma(acc[g][cb], a, zf[cb]);
+      }
     }
     __syncthreads();
 #pragma unroll
-    for (int cb = 0; cb < NC; ++cb) {
-      tile[w * 8 + lr][cb * 8 + 2 * lc] = acc[cb][0];
-      tile[w * 8 + lr][cb * 8 + 2 * lc + 1] = acc[cb][1];
-    }
+    for (int g = 0; g < RG; ++g)
+#pragma unroll
+      for (int cb = 0; cb < NC; ++cb) {
+        const int row = (g * (BJ_NT / 32) + w) * 8 + lr;
+        tile[row][cb * 8 + 2 * lc] = acc[g][cb][0];
+        tile[row][cb * 8 + 2 * lc + 1] = acc[g][cb][1];
+      }
     __syncthreads();
     const Chunk ch = chunk_at(c, B, brows, V, vrows);
     const int nr = min(BJ_CHUNK, ch.rows - ch.r0);
