@@ -727,6 +727,17 @@ void potrf_lower(Ctx& c, double* A, int dim, long long ld, int* info) {
   c.stats.chol_solves++;
 }
 
+namespace {
+__global__ void add_diag_kernel(double* A, int n, long long ld, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) A[(long long)i * ld + i] += v;
+}
+}  // namespace
+
+void add_diag(Ctx& c, double* A, int n, long long ld, double v) {
+  add_diag_kernel<<<cdiv(n, 256), 256, 0, c.stream>>>(A, n, ld, v);
+  QTT_CHECK_LAUNCH();
+}
+
 void potrs_lower(Ctx& c, const double* L, int dim, long long ld, double* b) {
   potrs_kernel<<<1, 1024, 0, c.stream>>>(L, dim, ld, b);
   QTT_CHECK_LAUNCH();

@@ -38,6 +38,8 @@ void svd(Ctx& c, CMatView in, MatView U, double* s, MatView Vt);
 // right-looking, DMMA trailing updates.  *info (device) = 0 on success, else
 // j+1 for the first non-positive pivot (LAPACK dpotrf convention).
 void potrf_lower(Ctx& c, double* A, int dim, long long ld, int* info);
+// A[i][i] += v for i < n (row-major, leading dimension ld)
+void add_diag(Ctx& c, double* A, int n, long long ld, double v);
 // Solve (L L^T) x = b in place, L from potrf_lower (dpotrs).
 void potrs_lower(Ctx& c, const double* L, int dim, long long ld, double* b);
 // *out = max_i sum_j |A[i,j]|   (Gershgorin bound, amen.py:190)

@@ -215,6 +215,7 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
   orthogonalize_rl(c, g);
   const auto t1 = now();
   double t_svd = 0.0;
+  int n_cert = 0;  // bonds split by the certified no-truncation path
   nrm2(c, g.cores[0].d.p, g.cores[0].numel(), c.scal);
   const double nrm = read1(c, c.scal);
   if (nrm == 0.0) {
@@ -232,6 +233,51 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
   for (int k = 0; k < K - 1; ++k) {
     Core& ck = g.cores[k];
     const int rows = ck.r0 * ck.m * ck.n, cols = ck.r1, kk = std::min(rows, cols);
+    // Certified no-truncation fast path (large tall unfoldings): with core = Q R (Householder),
+    // if G - tau I is positive definite (Cholesky succeeds) for G = R^T R and
+    // tau = delta^2 + 2 cols eps ||R||_F^2, then sigma_min(core)^2 >= delta^2 despite rounding
+    // (backward error of the Cholesky <= cols eps ||G||), so tt.py:386-393 keeps every
+    // singular value: r = cols, exactly the reference's decision.  The untruncated split
+    // U (S Vt) = core is then any orthogonal factorisation -- Q (R) -- the same tensor in
+    // another gauge, without the SVD.  Falls back to the SVD when the certificate fails.
+    if (cols >= 256 && rows >= cols && (max_rank <= 0 || max_rank >= cols) && old[k + 1] >= cols) {
+      const auto tq0 = now();
+      DBuf Q((long long)rows * cols, c.stream), R((long long)cols * cols, c.stream), G((long long)cols * cols, c.stream);
+      qr(c, crowmajor(ck.d.p, rows, cols), rowmajor(Q.p, rows, cols), rowmajor(R.p, cols, cols));
+      GemmArgs gg;  // G = R^T R
+      gg.M = cols; gg.N = cols; gg.K = cols;
+      gemm_set_A(gg, R.p, cols, true);
+      gemm_set_B(gg, R.p, cols, false);
+      gemm_set_C(gg, G.p, cols);
+      DBuf ws(gemm_workspace_hint(gg) + 1, c.stream);
+      gemm(gg, c.stream, ws.p, ws.n);
+      nrm2(c, R.p, (long long)cols * cols, c.scal + 2);
+      const double fro = read1(c, c.scal + 2);
+      const double tau = delta * delta + 2.0 * cols * 2.220446049250313e-16 * fro * fro;
+      add_diag(c, G.p, cols, cols, -tau);
+      potrf_lower(c, G.p, cols, cols, c.flags + 6);
+      int info = -1;
+      QTT_CUDA(cudaMemcpyAsync(&info, c.flags + 6, 4, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (info == 0) {
+        Core nk = make_core(c, ck.r0, ck.m, ck.n, cols);
+        QTT_CUDA(cudaMemcpyAsync(nk.d.p, Q.p, (size_t)rows * cols * 8, cudaMemcpyDeviceToDevice, c.stream));
+        Core& cn = g.cores[k + 1];
+        Core nn = make_core(c, cols, cn.m, cn.n, cn.r1);
+        GemmArgs h;  // R (cols x cols) @ next (cols x mn r1')
+        h.M = cols; h.N = cn.m * cn.n * cn.r1; h.K = cols;
+        gemm_set_A(h, R.p, cols, false);
+        gemm_set_B(h, cn.d.p, (long long)cn.m * cn.n * cn.r1, false);
+        gemm_set_C(h, nn.d.p, (long long)cn.m * cn.n * cn.r1);
+        gemm(h, c.stream);
+        g.cores[k] = std::move(nk);
+        g.cores[k + 1] = std::move(nn);
+        ++n_cert;
+        t_svd += std::chrono::duration<double>(now() - tq0).count();
+        continue;
+      }
+      t_svd += std::chrono::duration<double>(now() - tq0).count();
+    }
     DBuf U((long long)rows * kk, c.stream), s(kk, c.stream), Vt((long long)kk * cols, c.stream);
     const auto ts0 = now();
     svd(c, crowmajor(ck.d.p, rows, cols), rowmajor(U.p, rows, kk), s.p, rowmajor(Vt.p, kk, cols));
@@ -257,8 +303,8 @@ Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank) {
     g.cores[k + 1] = std::move(nn);
   }
   if (dbg)
-    std::fprintf(stderr, "[qtt] tt_round K=%d: orthogonalize %.3f s, svd %.3f s, total %.3f s\n", K,
-                 std::chrono::duration<double>(t1 - t0).count(), t_svd,
+    std::fprintf(stderr, "[qtt] tt_round K=%d: orthogonalize %.3f s, svd %.3f s (%d bonds certified untruncated), "
+                 "total %.3f s\n", K, std::chrono::duration<double>(t1 - t0).count(), t_svd, n_cert,
                  std::chrono::duration<double>(now() - t0).count());
   return g;
 }

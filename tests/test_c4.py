@@ -107,3 +107,19 @@ def test_gpu_round_config4_r32_vs_oracle():
     assert [c.shape for c in y.cores] == [c.shape for c in ref]
     diff = O.tt_norm(O.tt_sub(list(y.cores), ref))
     assert diff <= 1e-12 * O.tt_norm(ref)
+
+
+@pytest.mark.gpu
+def test_gpu_round_large_bond_truncating_vs_oracle():
+    """A rank-deficient large bond (x + x at bond 600 = 2 x 300): the certified no-truncation
+    path must refuse and the SVD path truncate to the oracle's ranks."""
+    from paper_2501_12151_b200 import tt
+    rng = np.random.default_rng(7)
+    dims = (2, 2, 2, 2, 2, 2, 2, 2, 2, 2)
+    ranks = [1, 2, 4, 8, 16, 300, 16, 8, 4, 2, 1]
+    x = [rng.standard_normal((ranks[k], 2, ranks[k + 1])) / np.sqrt(ranks[k]) for k in range(len(dims))]
+    xx = O.tt_add(x, x)
+    y = tt.tt_round(tt.TensorTrain(xx), tt.TruncationPolicy(1e-10))
+    ref = O.tt_round(xx, 1e-10)
+    assert [c.shape for c in y.cores] == [c.shape for c in ref]
+    assert O.tt_norm(O.tt_sub(list(y.cores), ref)) <= 1e-12 * O.tt_norm(ref)
