@@ -32,7 +32,8 @@ enum {
   QTT_ERR_SOLVER = 2,   /* SolverError        (errors.py:29) */
   QTT_ERR_CAPACITY = 3, /* CapacityError      (errors.py:13) -- device OOM */
   QTT_ERR_CUDA = 4,     /* CUDA runtime failure / no device                */
-  QTT_ERR_ARG = 5       /* ValueError: invalid argument                    */
+  QTT_ERR_ARG = 5,      /* ValueError: invalid argument                    */
+  QTT_ERR_FORMAT = 6    /* FormatError        (errors.py:33) -- bad QTT1 container */
 };
 
 typedef struct qtt_ctx qtt_ctx;
@@ -118,6 +119,12 @@ int qtt_train_info(const qtt_train* t, int* order, int* core_ndim, int64_t* nume
 int qtt_train_shape(const qtt_train* t, int64_t* shape);
 int qtt_train_download(qtt_ctx* ctx, const qtt_train* t, double* data);
 int qtt_train_free(qtt_train* t);
+/* QTT1 container (serialize.py:1-101; byte layout serialize.py:3-16) read straight into /
+ * written from a device-resident train.  is_operator (out) = 1 for kind 'O'.  Errors: the
+ * reference's FormatError cases (bad magic, unknown kind, truncated header / values,
+ * trailing bytes) -> QTT_ERR_FORMAT; rank chaining -> QTT_ERR_SHAPE. */
+int qtt_train_load_qtt1(qtt_ctx* ctx, const char* path, int* is_operator, qtt_train** out);  /* serialize.py:52 load_tt */
+int qtt_train_save_qtt1(qtt_ctx* ctx, const qtt_train* t, const char* path);                 /* serialize.py:33 save_tt */
 
 /* ---- TT algebra (tt.py) ----------------------------------------------------- */
 int qtt_orthogonalize_rl(qtt_ctx* ctx, const qtt_train* a, qtt_train** out); /* tt.py:396 */

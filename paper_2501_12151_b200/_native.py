@@ -11,7 +11,7 @@ import threading
 
 import numpy as np
 
-from .errors import CapacityError, DeviceError, ShapeMismatchError, SolverError
+from .errors import CapacityError, DeviceError, FormatError, ShapeMismatchError, SolverError
 
 # QTT_LIB overrides the library path (A/B timing of two builds on one GPU box)
 LIB_PATH = os.environ.get("QTT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtt.so")
@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("QTT_LIB") or os.path.join(os.path.dirname(os.path.abs
 _lib = None
 _lock = threading.Lock()
 
-QTT_OK, QTT_ERR_SHAPE, QTT_ERR_SOLVER, QTT_ERR_CAPACITY, QTT_ERR_CUDA, QTT_ERR_ARG = range(6)
+QTT_OK, QTT_ERR_SHAPE, QTT_ERR_SOLVER, QTT_ERR_CAPACITY, QTT_ERR_CUDA, QTT_ERR_ARG, QTT_ERR_FORMAT = range(7)
 
 _P = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.c_int
@@ -69,6 +69,8 @@ SIGNATURES = {
     "qtt_train_shape": [_VP, ctypes.POINTER(ctypes.c_int64)],
     "qtt_train_download": [_VP, _VP, _P],
     "qtt_train_free": [_VP],
+    "qtt_train_load_qtt1": [_VP, ctypes.c_char_p, ctypes.POINTER(_I), ctypes.POINTER(_VP)],
+    "qtt_train_save_qtt1": [_VP, _VP, ctypes.c_char_p],
     "qtt_orthogonalize_rl": [_VP, _VP, ctypes.POINTER(_VP)],
     "qtt_tt_norm": [_VP, _VP, _P],
     "qtt_tt_dot": [_VP, _VP, _VP, _P],
@@ -135,6 +137,8 @@ def check(code: int):
         raise SolverError(msg)
     if code == QTT_ERR_CAPACITY:
         raise CapacityError(msg)
+    if code == QTT_ERR_FORMAT:
+        raise FormatError(msg)
     if code == QTT_ERR_ARG:
         raise ValueError(msg)
     raise DeviceError(msg)

@@ -1,6 +1,9 @@
 // extern "C" boundary, part 2: device-resident trains, TT algebra, dense
 // factorizations and the AMEn solve (include/qtt.h).
 #include <cmath>
+#include <vector>
+#include <cstring>
+#include <cstdio>
 #include <string>
 
 #include "../../include/qtt.h"
@@ -118,6 +121,86 @@ int qtt_train_download(qtt_ctx* ctx, const qtt_train* t, double* data) {
       off += core.numel();
     }
     c.sync();
+  });
+}
+
+int qtt_train_load_qtt1(qtt_ctx* ctx, const char* path, int* is_operator, qtt_train** out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (!path || !out) throw qtt::Error(QTT_ERR_ARG, "null path/out");
+    const std::string p(path);
+    FILE* fh = std::fopen(path, "rb");
+    if (!fh) throw qtt::Error(QTT_ERR_ARG, p + ": cannot open");
+    std::vector<unsigned char> data;
+    {
+      unsigned char buf[1 << 16];
+      size_t got;
+      while ((got = std::fread(buf, 1, sizeof(buf), fh)) > 0) data.insert(data.end(), buf, buf + got);
+      std::fclose(fh);
+    }
+    auto u32 = [&](size_t off) {
+      return (uint32_t)data[off] | ((uint32_t)data[off + 1] << 8) | ((uint32_t)data[off + 2] << 16) |
+             ((uint32_t)data[off + 3] << 24);
+    };
+    if (data.size() < 9 || std::memcmp(data.data(), "QTT1", 4) != 0)
+      throw qtt::Error(QTT_ERR_FORMAT, p + ": not a QTT1 container (bad magic)");
+    const unsigned char kind = data[4];
+    if (kind != 'V' && kind != 'O') throw qtt::Error(QTT_ERR_FORMAT, p + ": unknown kind tag");
+    const uint32_t count = u32(5);
+    size_t off = 9;
+    qtt::Train t;
+    t.is_op = kind == 'O';
+    for (uint32_t k = 0; k < count; ++k) {
+      if (off + 16 > data.size())
+        throw qtt::Error(QTT_ERR_FORMAT, p + ": truncated header of core " + std::to_string(k));
+      const uint32_t d0 = u32(off), d1 = u32(off + 4), d2 = u32(off + 8), d3 = u32(off + 12);
+      off += 16;
+      const unsigned long long size = (unsigned long long)d0 * d1 * d2 * d3;
+      if (off + 8 * size > data.size())
+        throw qtt::Error(QTT_ERR_FORMAT, p + ": truncated values of core " + std::to_string(k));
+      if (d0 < 1 || d1 < 1 || d2 < 1 || d3 < 1 || (!t.is_op && d2 != 1))
+        throw qtt::Error(QTT_ERR_SHAPE, p + ": invalid core dims at core " + std::to_string(k));
+      qtt::Core core = qtt::make_core(c, (int)d0, (int)d1, (int)d2, (int)d3);
+      // little-endian binary64 on a little-endian host: a straight copy (upload is stream-ordered
+      // and the host vector outlives it: synchronized below)
+      core.d.upload(reinterpret_cast<const double*>(data.data() + off), (long long)size);
+      off += 8 * size;
+      t.cores.push_back(std::move(core));
+    }
+    if (off != data.size())
+      throw qtt::Error(QTT_ERR_FORMAT, p + ": " + std::to_string(data.size() - off) + " trailing bytes");
+    c.sync();
+    check_chain(t);
+    if (is_operator) *is_operator = t.is_op ? 1 : 0;
+    *out = wrap(std::move(t));
+  });
+}
+
+int qtt_train_save_qtt1(qtt_ctx* ctx, const qtt_train* th, const char* path) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& t = T(th);
+    std::vector<unsigned char> out;
+    auto put32 = [&](uint32_t v) {
+      for (int i = 0; i < 4; ++i) out.push_back((unsigned char)((v >> (8 * i)) & 0xff));
+    };
+    out.insert(out.end(), {'Q', 'T', 'T', '1', (unsigned char)(t.is_op ? 'O' : 'V')});
+    put32((uint32_t)t.cores.size());
+    for (const auto& k : t.cores) {
+      put32((uint32_t)k.r0);
+      put32((uint32_t)k.m);
+      put32((uint32_t)k.n);
+      put32((uint32_t)k.r1);
+      const size_t at = out.size();
+      out.resize(at + 8 * (size_t)k.numel());
+      QTT_CUDA(cudaMemcpyAsync(out.data() + at, k.d.p, 8 * (size_t)k.numel(), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();  // (out may reallocate on the next resize)
+    }
+    FILE* fh = std::fopen(path, "wb");
+    if (!fh) throw qtt::Error(QTT_ERR_ARG, std::string(path) + ": cannot open for writing");
+    const size_t w = std::fwrite(out.data(), 1, out.size(), fh);
+    std::fclose(fh);
+    if (w != out.size()) throw qtt::Error(QTT_ERR_ARG, std::string(path) + ": short write");
   });
 }
 

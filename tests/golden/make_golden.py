@@ -297,11 +297,25 @@ def c4_cases():
     return d
 
 
+def qtt1_cases():
+    """Reference QTT1 containers (serialize.py:33-49) of a small vector and operator."""
+    import ttfem.serialize as rser
+    rng = np.random.default_rng(5)
+    v = rtt.TensorTrain(rand_train(rng, (3, 2, 2, 2), [2, 3, 2]))
+    a = rtt.TTLinearOperator(rand_op(rng, (3, 2, 2), [2, 3]))
+    rser.save_tt(v, os.path.join(HERE, "vec.qtt1"))
+    rser.save_tt(a, os.path.join(HERE, "op.qtt1"))
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "qtt1":
+        qtt1_cases()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "c4":  # regenerate only the config-4 fixture
         np.savez_compressed(os.path.join(HERE, "c4_small.npz"), **c4_cases())
         return
     np.savez_compressed(os.path.join(HERE, "c4_small.npz"), **c4_cases())
+    qtt1_cases()
     np.savez_compressed(os.path.join(HERE, "kernels_bin.npz"), **kernels_case(1, (2,) * 8, 12, 6, 4))
     np.savez_compressed(os.path.join(HERE, "kernels_lead3.npz"), **kernels_case(2, (3,) + (2,) * 7, 10, 7, 4))
     np.savez_compressed(os.path.join(HERE, "factor.npz"), **factor_cases())
