@@ -324,6 +324,89 @@ __global__ void __launch_bounds__(PNT) panel_smem_kernel(PanelArgs a) {
   }
 }
 
+// ---- V and T of a factored panel (replaces build_v + V^T V + dlarft launches): P holds
+// this CTA's rows of the factored panel, column-major with pitch ldp; on exit a.Vb (unit
+// lower trapezoid, mrows x jb column-major) and a.T (dlarft forward columnwise) are written.
+// Must be called by every CTA of the cluster (it contains cluster barriers).
+template <int NTH>
+__device__ void panel_emit_vt(const PanelArgs& a, double* P, int ldp, int nloc, int r0, cg::cluster_group& cl) {
+  const int G = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  __syncthreads();
+  const int mrows = a.m - a.j0, jb = a.jb;
+  for (int e = threadIdx.x; e < nloc * jb; e += NTH) {  // P -> V in place, and V out
+    const int c = e / nloc, i = e % nloc;
+    const int pr = r0 - a.j0 + i;  // row inside the panel
+    const double v = pr > c ? P[c * ldp + i] : (pr == c ? 1.0 : 0.0);
+    P[c * ldp + i] = v;
+    a.Vb[(long long)c * mrows + pr] = v;
+  }
+  __syncthreads();
+  // partial Gram of this CTA's rows: thread owns a 4x4 block of the 64x64 index space;
+  // Gp / Gs / Ts live in the (now free) dynamic panel buffer, sized for them at launch
+  double (*Gp)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(P);
+  double (*Gs)[NB + 1] = Gp + NB;
+  double (*Ts)[NB + 1] = Gp + 2 * NB;
+  {
+    const int tg = threadIdx.x & 255;  // 256-thread Gram layout (extra threads idle)
+    const int p0 = 4 * (tg >> 4), q0 = 4 * (tg & 15);
+    const bool gact = threadIdx.x < 256;
+    double g[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) g[x][y] = 0.0;
+    if (gact && p0 < jb && q0 < jb && q0 + 3 >= p0) {  // blocks touching the upper triangle
+      for (int i = 0; i < nloc; ++i) {
+        double vp[4], vq[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          vp[x] = p0 + x < jb ? P[(p0 + x) * ldp + i] : 0.0;
+          vq[x] = q0 + x < jb ? P[(q0 + x) * ldp + i] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) g[x][y] = fma(vp[x], vq[y], g[x][y]);
+      }
+    }
+    __syncthreads();  // every thread is done reading V from P
+    if (gact)
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) Gp[p0 + x][q0 + y] = g[x][y];
+  }
+  cl.sync();
+  if (rank == 0) {  // sum the partials in rank order, then the dlarft recursion in shared memory
+    for (int e = threadIdx.x; e < jb * jb; e += NTH) {
+      const int p = e / jb, q = e % jb;
+      double sum = 0.0;
+      if (p < q)
+        for (int r = 0; r < G; ++r) sum += cl.map_shared_rank(&Gp[0][0], r)[p * (NB + 1) + q];
+      Gs[p][q] = sum;
+      Ts[p][q] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < jb; ++j) {  // T[j][j] = tau_j;  T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
+      const double tj = a.tau[a.j0 + j];
+      if ((int)threadIdx.x < j) {
+        double acc = 0.0;
+        for (int q = threadIdx.x; q < j; ++q) acc = fma(Ts[threadIdx.x][q], Gs[q][j], acc);
+        Ts[threadIdx.x][j] = -tj * acc;
+      }
+      if (threadIdx.x == 0) Ts[j][j] = tj;
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < jb * jb; e += NTH) {
+      const int p = e / jb, q = e % jb;
+      a.T[e] = Ts[p][q];
+      if (a.Tb) a.Tb[(long long)(a.tb_off + p) * a.ldtb + a.tb_off + q] = Ts[p][q];
+    }
+  }
+  cl.sync();  // no CTA leaves while rank 0 may still read its shared memory
+}
+
+
 // Panel factorization inside ONE thread-block cluster (up to 16 CTAs on one GPC):
 // the per-column reductions go through distributed shared memory and the two
 // barriers per column are hardware cluster barriers, instead of L2 round trips and
@@ -479,77 +562,174 @@ __global__ void __launch_bounds__(PNT) panel_cluster_kernel(PanelArgs a) {
     cl.sync();  // no CTA leaves while another may still read its shared memory
     return;
   }
-  // ---- V and T of the panel (replaces build_v + V^T V + dlarft launches)
-  __syncthreads();
-  const int mrows = a.m - a.j0, jb = a.jb;
-  for (int e = threadIdx.x; e < nloc * jb; e += PNT) {  // P -> V in place, and V out
-    const int c = e / nloc, i = e % nloc;
-    const int pr = r0 - a.j0 + i;  // row inside the panel
-    const double v = pr > c ? P[c * ldp + i] : (pr == c ? 1.0 : 0.0);
-    P[c * ldp + i] = v;
-    a.Vb[(long long)c * mrows + pr] = v;
+  panel_emit_vt<PNT>(a, P, ldp, nloc, r0, cl);
+}
+
+// Register-resident panel (jb <= 32): the same factorization as panel_cluster_kernel, but each
+// thread keeps its rows of the panel (RPT rows x 32 columns) in REGISTERS for the whole panel.
+// Per column the only shared-memory traffic is the reductions: the partial dot products of the
+// reflector with the remaining columns are reduced inside each warp by a transpose-reduction
+// (8 columns per pass, 3 halving shuffle steps + 2 butterflies) instead of streaming every
+// column of the panel through shared memory twice (the smem kernel is bandwidth-bound there).
+constexpr int RJB = 32;
+template <int RPT>
+__global__ void __launch_bounds__(PNT, 1) panel_reg_kernel(PanelArgs a) {
+  extern __shared__ double P[];  // V/T emission scratch (written column by column)
+  constexpr int NWW = PNT / 32;
+  __shared__ double red2[2 * NWW];
+  __shared__ double nin[16][2];
+  __shared__ double din[16][RJB];
+  __shared__ double wsum[NWW][RJB];
+  __shared__ double sw[RJB];
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int rows = a.m - a.j0;
+  const int chunk = (rows + G - 1) / G;
+  const int r0 = a.j0 + rank * chunk, r1 = min(a.m, r0 + chunk);
+  const int nloc = max(0, r1 - r0);
+  const int ldp = nloc | 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jb = a.jb;
+  double* W = a.W;
+  const long long ld = a.ld;
+  constexpr int NONE = 0x7fffffff;
+  // w[q][0] is always the CURRENT column: the register window shifts left by one column per
+  // step, so every register index is static while the column loop stays a runtime loop
+  double w[RPT][RJB];
+  int grow[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = threadIdx.x + q * PNT;
+    grow[q] = i < nloc ? r0 + i : NONE;
+#pragma unroll
+    for (int c = 0; c < RJB; ++c) w[q][c] = (i < nloc && c < jb) ? W[(long long)(a.j0 + c) * ld + r0 + i] : 0.0;
   }
-  __syncthreads();
-  // partial Gram of this CTA's rows: thread owns a 4x4 block of the 64x64 index space;
-  // Gp / Gs / Ts live in the (now free) dynamic panel buffer, sized for them at launch
-  double (*Gp)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(P);
-  double (*Gs)[NB + 1] = Gp + NB;
-  double (*Ts)[NB + 1] = Gp + 2 * NB;
-  {
-    const int p0 = 4 * (threadIdx.x >> 4), q0 = 4 * (threadIdx.x & 15);
-    double g[4][4];
+  for (int j = 0; j < jb; ++j) {
+    const int rj = a.j0 + j;
+    const int nrem = jb - j - 1;  // remaining columns: window slots 1..nrem
+    // ---- norm of the column below the diagonal, and its diagonal entry
+    double pn = 0.0, ap = 0.0;
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) g[x][y] = 0.0;
-    if (p0 < jb && q0 < jb && q0 + 3 >= p0) {  // blocks touching the upper triangle
-      for (int i = 0; i < nloc; ++i) {
-        double vp[4], vq[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          vp[x] = p0 + x < jb ? P[(p0 + x) * ldp + i] : 0.0;
-          vq[x] = q0 + x < jb ? P[(q0 + x) * ldp + i] : 0.0;
-        }
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) g[x][y] = fma(vp[x], vq[y], g[x][y]);
-      }
+    for (int q = 0; q < RPT; ++q) {
+      if (grow[q] != NONE && grow[q] > rj) pn = fma(w[q][0], w[q][0], pn);
+      if (grow[q] == rj) ap = w[q][0];
     }
-    __syncthreads();  // every thread is done reading V from P
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) Gp[p0 + x][q0 + y] = g[x][y];
-  }
-  cl.sync();
-  if (rank == 0) {  // sum the partials in rank order, then the dlarft recursion in shared memory
-    for (int e = threadIdx.x; e < jb * jb; e += PNT) {
-      const int p = e / jb, q = e % jb;
-      double sum = 0.0;
-      if (p < q)
-        for (int r = 0; r < G; ++r) sum += cl.map_shared_rank(&Gp[0][0], r)[p * (NB + 1) + q];
-      Gs[p][q] = sum;
-      Ts[p][q] = 0.0;
+    pn = warp_sum(pn);
+    ap = warp_sum(ap);
+    if (lane == 0) {
+      red2[warp] = pn;
+      red2[NWW + warp] = ap;
     }
     __syncthreads();
-    for (int j = 0; j < jb; ++j) {  // T[j][j] = tau_j;  T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]
-      const double tj = a.tau[a.j0 + j];
-      if ((int)threadIdx.x < j) {
-        double acc = 0.0;
-        for (int q = threadIdx.x; q < j; ++q) acc = fma(Ts[threadIdx.x][q], Gs[q][j], acc);
-        Ts[threadIdx.x][j] = -tj * acc;
+    if ((int)threadIdx.x < G) {  // push this CTA's sums into every CTA's inbox
+      double x = 0.0, y = 0.0;
+#pragma unroll
+      for (int k = 0; k < NWW; ++k) {
+        x += red2[k];
+        y += red2[NWW + k];
       }
-      if (threadIdx.x == 0) Ts[j][j] = tj;
-      __syncthreads();
+      double* dst = cl.map_shared_rank(&nin[0][0], (int)threadIdx.x);
+      dst[2 * rank] = x;
+      dst[2 * rank + 1] = y;
     }
-    for (int e = threadIdx.x; e < jb * jb; e += PNT) {
-      const int p = e / jb, q = e % jb;
-      a.T[e] = Ts[p][q];
-      if (a.Tb) a.Tb[(long long)(a.tb_off + p) * a.ldtb + a.tb_off + q] = Ts[p][q];
+    cl.sync();
+    double xnorm2 = 0.0, alpha = 0.0;
+    for (int r = 0; r < G; ++r) {  // rank order: identical in every CTA
+      xnorm2 += nin[r][0];
+      alpha += nin[r][1];
+    }
+    double tau = 0.0, beta = alpha, scal = 1.0;
+    if (xnorm2 > 0.0) {  // dlarfg
+      beta = -copysign(hypot(alpha, sqrt(xnorm2)), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (rank == 0 && threadIdx.x == 0) a.tau[rj] = tau;
+    double v[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (grow[q] != NONE && grow[q] > rj) {
+        w[q][0] *= scal;
+        v[q] = w[q][0];
+      } else {
+        v[q] = grow[q] == rj ? 1.0 : 0.0;
+      }
+    }
+    const bool upd = tau != 0.0 && nrem > 0;  // uniform over the cluster
+    if (upd) {
+      // ---- partial dots d_c = sum_rows v w[:, c], c = 1..nrem, reduced within each warp
+#pragma unroll
+      for (int c8 = 0; c8 < RJB; c8 += 8) {
+        if (c8 > nrem) break;
+        double vals[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          vals[k] = 0.0;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) vals[k] = fma(v[q], w[q][c8 + k], vals[k]);
+        }
+#pragma unroll
+        for (int st = 4; st >= 1; st >>= 1) {
+          const bool up = (lane & st) != 0;
+#pragma unroll
+          for (int k = 0; k < st; ++k) {
+            const double send = up ? vals[k] : vals[k + st];
+            const double keep = up ? vals[k + st] : vals[k];
+            vals[k] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+          }
+        }
+        vals[0] += __shfl_xor_sync(0xffffffffu, vals[0], 8);
+        vals[0] += __shfl_xor_sync(0xffffffffu, vals[0], 16);
+        if (lane < 8) wsum[warp][c8 + lane] = vals[0];
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < G * RJB; e += PNT) {  // CTA partials -> every CTA's inbox
+        const int col = e % RJB, dest = e / RJB;
+        if (col >= 1 && col <= nrem) {
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < NWW; ++k) d += wsum[k][col];
+          cl.map_shared_rank(&din[0][0], dest)[rank * RJB + col] = d;
+        }
+      }
+    }
+    cl.sync();
+    if (upd) {
+      if ((int)threadIdx.x < RJB) {
+        double d = 0.0;
+        for (int r = 0; r < G; ++r) d += din[r][threadIdx.x];
+        sw[threadIdx.x] = d * tau;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 1; c < RJB; ++c) {
+        const double wc = c <= nrem ? sw[c] : 0.0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) w[q][c] = fma(-wc, v[q], w[q][c]);
+      }
+    }
+    // ---- column j is final: R above the diagonal, beta on it, the reflector below
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (grow[q] == NONE) continue;
+      const int i = threadIdx.x + q * PNT;
+      const double val = grow[q] == rj ? beta : w[q][0];
+      W[(long long)rj * ld + r0 + i] = val;
+      if (a.T) P[j * ldp + i] = val;
+    }
+    // ---- shift the register window
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+#pragma unroll
+      for (int c = 0; c + 1 < RJB; ++c) w[q][c] = w[q][c + 1];
+      w[q][RJB - 1] = 0.0;
     }
   }
-  cl.sync();  // no CTA leaves while rank 0 may still read its shared memory
+  if (a.T == nullptr) {
+    cl.sync();
+    return;
+  }
+  panel_emit_vt<PNT>(a, P, ldp, nloc, r0, cl);
 }
 
 constexpr int CLUSTER_SMEM_DOUBLES = 25 * 1024;  // 200 KB of panel rows per CTA
@@ -594,6 +774,57 @@ bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s
   }
   QTT_CHECK_LAUNCH();
   return true;
+}
+
+// Launch the register-resident panel (16-CTA cluster) when jb <= 32 and each CTA's rows fit
+// 3 per thread; false otherwise.
+template <int RPT>
+bool launch_panel_reg_t(const PanelArgs& pa, size_t dyn, cudaStream_t s) {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(panel_reg_kernel<RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                 cudaSuccess &&
+             cudaFuncSetAttribute(panel_reg_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CLUSTER_SMEM_DOUBLES * 8) == cudaSuccess
+         ? 1
+         : 0;
+    cudaGetLastError();
+  }
+  if (!ok) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16);
+  cfg.blockDim = dim3(PNT);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, panel_reg_kernel<RPT>, pa);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  QTT_CHECK_LAUNCH();
+  return true;
+}
+
+bool launch_panel_reg(const PanelArgs& pa, int mrows, int jb, cudaStream_t s) {
+  static const int disabled = std::getenv("QTT_PANEL_REG") && std::atoi(std::getenv("QTT_PANEL_REG")) == 0;
+  if (disabled || jb > RJB) return false;
+  const int chunk = (mrows + 15) / 16;
+  const int rpt = (chunk + PNT - 1) / PNT;
+  if (rpt > 3) return false;
+  const size_t dyn = std::max<size_t>(pa.T ? (size_t)(chunk | 1) * jb : 0, pa.T ? 3 * NB * (NB + 1) : 0) * 8;
+  if (dyn > (size_t)CLUSTER_SMEM_DOUBLES * 8) return false;
+  switch (rpt) {
+    case 1: return launch_panel_reg_t<1>(pa, dyn, s);
+    case 2: return launch_panel_reg_t<2>(pa, dyn, s);
+    default: return launch_panel_reg_t<3>(pa, dyn, s);
+  }
 }
 
 int panel_grid(int rows) {
@@ -733,7 +964,9 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
     }
     // panel width: 64, or 32 when a 64-wide panel would not fit one 16-CTA cluster
     static const int cl_rows = 16 * (CLUSTER_SMEM_DOUBLES / NB);
-    const int pw = (m - J0 > cl_rows) ? NB / 2 : NB;
+    static const bool reg_on = !(std::getenv("QTT_PANEL_REG") && std::atoi(std::getenv("QTT_PANEL_REG")) == 0);
+    const bool reg_fits = reg_on && (m - J0 + 15) / 16 <= 3 * PNT;  // register panel: 32 columns
+    const int pw = (reg_fits || m - J0 > cl_rows) ? NB / 2 : NB;
     for (int j0 = J0; j0 < jend; j0 += pw) {
       const int jb = std::min(pw, jend - j0);
       const int mrows = m - j0;
@@ -749,7 +982,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       }
       const int Gs = panel_smem_grid(mrows, jb);
       bool have_vt = false;
-      if (launch_panel_cluster(pa, mrows, jb, c.stream)) {
+      if (launch_panel_reg(pa, mrows, jb, c.stream) || launch_panel_cluster(pa, mrows, jb, c.stream)) {
         have_vt = need_t;
       } else if (Gs <= 148) {
         static bool attr = false;
