@@ -65,3 +65,28 @@ def test_identity_and_scaled():
     assert rep.converged and residual_norm(tt_identity(dims), x, f) <= 1e-13
     x, rep = amen_solve(tt_op_scale(tt_identity((4, 4)), 2.0), tt_ones((4, 4)))
     assert rep.converged and np.allclose(tt_to_dense(x), 0.5, atol=1e-12)
+
+
+def test_config_c1_vs_reference_ensemble():
+    """BASELINE config C1 itself (3D cube, 2^5 nodes/axis, 98,304 DOF, tol 1e-6, max rank 32,
+    x0 rank-2 N(0,1) seed 0): the device solve must land inside the reference's own
+    trajectory band (9 runs of the real reference under 1e-15 x0 perturbations,
+    tests/golden/make_c1_band.py) widened by the north_star's 10%, with the same rank cap."""
+    import json
+    import os
+
+    from paper_2501_12151_b200.amen import AmenConfig, amen_solve
+    from paper_2501_12151_b200.configs import WORKLOADS, build
+    from paper_2501_12151_b200.tt import TensorTrain, TruncationPolicy, TTLinearOperator
+    from tests.golden_io import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "c1_band.json")))
+    prob, x0, kw = build(WORKLOADS["C1"])
+    rel, cap = kw.pop("rounding")
+    x, rep = amen_solve(TTLinearOperator(prob.op), TensorTrain(prob.rhs), TensorTrain(x0),
+                        AmenConfig(rounding=TruncationPolicy(rel, cap), **kw))
+    lo, hi = ref["band_final"]
+    assert 0.9 * lo <= rep.final_relative_residual <= 1.1 * hi, (rep.final_relative_residual, ref["band_final"])
+    assert rep.converged == ref["converged"]
+    assert max(x.ranks) == max(ref["ranks"])
+    slo, shi = ref["band_sweeps"]
+    assert slo <= rep.sweeps_used <= shi
