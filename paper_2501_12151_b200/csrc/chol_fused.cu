@@ -39,9 +39,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // Factor the nb x nb diagonal block at (j0, j0) in shared memory s (stride LD), one
-// CTA; the trailing updates use a 16x16 thread map (no per-element div/mod).
+// CTA, blocked by PW = 8 columns: warp 0 factors each 8-column panel (rows k0..nb-1, two
+// rows per lane, warp-synchronous: pivots and multipliers travel by shuffles, no block
+// barrier), then all threads apply the rank-8 update to the trailing lower triangle.
 // Returns 0 or the 1-based failing column (global index).
 __device__ int factor_diag(double* A, long long ld, int j0, int nb, double* s) {
+  constexpr int PW = 8;
   for (int e = threadIdx.x; e < nb * nb; e += NT) {
     const int i = e / nb, j = e % nb;
     s[i * LD + j] = (j <= i) ? __ldcg(A + (long long)(j0 + i) * ld + j0 + j) : 0.0;
@@ -49,22 +52,64 @@ __device__ int factor_diag(double* A, long long ld, int j0, int nb, double* s) {
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  for (int j = 0; j < nb; ++j) {
-    const double d = s[j * LD + j];
-    if (!(d > 0.0)) {  // dpotrf: non-positive or NaN pivot
-      if (threadIdx.x == 0) bad = j0 + j + 1;
-      __syncthreads();
-      break;
+  for (int k0 = 0; k0 < nb; k0 += PW) {
+    const int pw = min(PW, nb - k0);
+    if (warp == 0) {
+      const int ra = k0 + lane, rb = k0 + 32 + lane;  // this lane's panel rows
+      double v[2][PW];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        v[0][c] = (ra < nb && c < pw) ? s[ra * LD + k0 + c] : 0.0;
+        v[1][c] = (rb < nb && c < pw) ? s[rb * LD + k0 + c] : 0.0;
+      }
+      int fail = 0;
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        if (c < pw && fail == 0) {
+          const double d = __shfl_sync(0xffffffffu, v[0][c], c);  // row k0 + c lives in lane c
+          if (!(d > 0.0)) {
+            fail = j0 + k0 + c + 1;  // dpotrf: non-positive or NaN pivot
+          } else {
+            const double l = sqrt(d), inv = 1.0 / l;
+            if (ra > k0 + c) v[0][c] *= inv;
+            if (ra == k0 + c) v[0][c] = l;
+            if (rb < nb) v[1][c] *= inv;
+#pragma unroll
+            for (int c2 = c + 1; c2 < PW; ++c2) {
+              const double m = __shfl_sync(0xffffffffu, v[0][c], c2);  // L[k0 + c2][c]
+              if (c2 < pw) {
+                if (ra >= k0 + c2) v[0][c2] = fma(-v[0][c], m, v[0][c2]);
+                if (rb < nb) v[1][c2] = fma(-v[1][c], m, v[1][c2]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        if (c < pw) {
+          if (ra < nb && ra >= k0 + c) s[ra * LD + k0 + c] = v[0][c];
+          if (rb < nb) s[rb * LD + k0 + c] = v[1][c];
+        }
+      }
+      if (lane == 0 && fail != 0) bad = fail;
     }
-    const double ljj = sqrt(d), inv = 1.0 / ljj;
-    // scale column j below the diagonal (rows j+1..nb-1); diagonal written after
-    for (int i = j + 1 + threadIdx.x; i < nb; i += NT) s[i * LD + j] *= inv;
     __syncthreads();
-    if (threadIdx.x == 0) s[j * LD + j] = ljj;
-    for (int i = j + 1 + ty; i < nb; i += 16) {
-      const double lij = s[i * LD + j];
-      for (int c = j + 1 + tx; c <= i; c += 16) s[i * LD + c] -= lij * s[c * LD + j];
+    if (bad != 0) break;  // uniform
+    // rank-pw update of the trailing lower triangle: rows/cols >= k0 + pw
+    const int t0 = k0 + pw;
+    for (int i = t0 + ty; i < nb; i += 16) {
+      double li[PW];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) li[c] = c < pw ? s[i * LD + k0 + c] : 0.0;
+      for (int jc = t0 + tx; jc <= i; jc += 16) {
+        double acc = s[i * LD + jc];
+#pragma unroll
+        for (int c = 0; c < PW; ++c) acc = fma(-li[c], s[jc * LD + k0 + c], acc);
+        s[i * LD + jc] = acc;
+      }
     }
     __syncthreads();
   }
@@ -79,26 +124,36 @@ __device__ int factor_diag(double* A, long long ld, int j0, int nb, double* s) {
 }
 
 // Linv (NB x NB row-major, zero above the diagonal) = inverse of the lower-triangular
-// nb x nb block in shared memory s: one thread per column, forward substitution.
+// nb x nb block in shared memory s: forward substitution, 4 lanes per column (each lane
+// owns every 4th row of the column's solution in registers; the partial dot products of
+// a row are combined with two shuffles).  Requires NT == 4 * NB.
 __device__ void invert_lower(const double* s, int nb, double* Linv) {
-  const int c = threadIdx.x;
-  if (c < NB) {
-    double x[NB];
+  static_assert(NT == 4 * NB, "4 lanes per column");
+  __shared__ double rdiag[NB];
+  if (threadIdx.x < NB) rdiag[threadIdx.x] = threadIdx.x < nb ? 1.0 / s[threadIdx.x * LD + threadIdx.x] : 0.0;
+  __syncthreads();
+  const int c = threadIdx.x >> 2, part = threadIdx.x & 3;
+  double xs[NB / 4];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      double v = (i == c) ? 1.0 : 0.0;
-      if (i < nb && i >= c) {
+  for (int k = 0; k < NB / 4; ++k) xs[k] = 0.0;
 #pragma unroll
-        for (int p = 0; p < i; ++p)
-          if (p >= c) v -= s[i * LD + p] * x[p];
-        x[i] = v / s[i * LD + i];
-      } else {
-        x[i] = 0.0;
-      }
+  for (int i = 0; i < NB; ++i) {
+    double a0 = 0.0, a1 = 0.0;  // two independent FMA chains
+#pragma unroll
+    for (int k = 0; k < NB / 4; k += 2) {
+      const int p0 = part + 4 * k, p1 = p0 + 4;
+      if (p0 < i && p0 >= c) a0 = fma(s[i * LD + p0], xs[k], a0);
+      if (p1 < i && p1 >= c) a1 = fma(s[i * LD + p1], xs[k + 1], a1);
     }
-#pragma unroll
-    for (int i = 0; i < NB; ++i) Linv[i * NB + c] = x[i];
+    double acc = a0 + a1;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    double xi = 0.0;
+    if (i < nb && i >= c) xi = ((i == c ? 1.0 : 0.0) - acc) * rdiag[i];
+    if (part == (i & 3)) xs[i >> 2] = xi;
   }
+#pragma unroll
+  for (int k = 0; k < NB / 4; ++k) Linv[(part + 4 * k) * NB + c] = xs[k];
   __syncthreads();
 }
 
@@ -131,56 +186,49 @@ __global__ void __launch_bounds__(NT) chol_fused_kernel(CholArgs a) {
   grid.sync();
   mark(0);
 
-  // ---- blocked right-looking Cholesky
+  // ---- blocked right-looking Cholesky with look-ahead.  Step j: (panel) every CTA forms
+  // L21 = A21 Linv_j^T for its 64-row blocks as DMMA tiles (Linv_j = L11^-1 from the
+  // diagonal factor), barrier, (trailing) A22 -= L21 L21^T on the lower tiles -- and CTA 0
+  // first updates the NEXT diagonal tile and factors + inverts it right away, so the next
+  // step's diagonal factor overlaps this step's trailing update instead of running alone.
+  if (blockIdx.x == 0) {
+    const int b = factor_diag(A, ld, 0, min(NB, dim), smem);
+    if (threadIdx.x == 0 && b != 0) *a.info = b;
+    mark(1);
+    if (b == 0) invert_lower(smem, min(NB, dim), a.Linv);
+    mark(4);
+  }
+  grid.sync();
   for (int j0 = 0; j0 < dim; j0 += NB) {
+    if (__ldcg(a.info) != 0) return;  // uniform: every CTA reads the same flag
+    const int bk = j0 / NB;
     const int nb = min(NB, dim - j0);
     const int rest = dim - j0 - nb;
-    if (blockIdx.x == 0) {
-      const int b = factor_diag(A, ld, j0, nb, smem);
-      if (threadIdx.x == 0 && b != 0) *a.info = b;
-    }
-    grid.sync();
-    mark(1);
-    if (__ldcg(a.info) != 0) return;  // uniform: every CTA reads the same flag
     if (rest <= 0) break;
-    // panel solve: L21 = A21 L11^-T, one thread per row, L11 staged in shared memory
+    // panel: L21 = A21 Linv^T  (B(k, n) = Linv[n][k])
     {
-      double* L = smem;
-      for (int e = threadIdx.x; e < nb * nb; e += NT) {
-        const int i = e / nb, j = e % nb;
-        L[i * LD + j] = (j <= i) ? __ldcg(A + (long long)(j0 + i) * ld + j0 + j) : 0.0;
+      const double* Li = a.Linv + (long long)bk * NB * NB;
+      double* A21 = A + (long long)(j0 + nb) * ld + j0;
+      const int rtiles = (rest + NB - 1) / NB;
+      tile::Operands o{A21, ld, 1, Li, 1, NB, rest, nb, nb};
+      for (int t = blockIdx.x; t < rtiles; t += gridDim.x) {
+        double acc[CF::MI][CF::NI][2];
+        tile::zero_acc<CF>(acc);
+        tile::mma_tile<CF>(o, t * NB, 0, 0, (nb + CF::BK - 1) / CF::BK, smem, acc);
+        tile::for_each_acc<CF>(t * NB, 0, rest, nb, acc,
+                               [&](int r, int c, double v) { A21[(long long)r * ld + c] = v; });
       }
-      __syncthreads();
-      for (int row = j0 + nb + blockIdx.x * NT + threadIdx.x; row < dim; row += gridDim.x * NT) {
-        double x[NB];
-        double* ar = A + (long long)row * ld + j0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) x[j] = j < nb ? ar[j] : 0.0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          if (j < nb) {
-            double v = x[j];
-#pragma unroll
-            for (int p = 0; p < j; ++p) v -= x[p] * L[j * LD + p];
-            x[j] = v / L[j * LD + j];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (j < nb) ar[j] = x[j];
-      }
-      __syncthreads();
     }
     grid.sync();
     mark(2);
-    // trailing update  A22 -= L21 L21^T  on lower tiles (DMMA)
+    // trailing update  A22 -= L21 L21^T  on lower tiles (DMMA); item 0 = next diagonal tile
     {
       const double* L21 = A + (long long)(j0 + nb) * ld + j0;
       double* A22 = A + (long long)(j0 + nb) * ld + j0 + nb;
       const int tiles = (rest + NB - 1) / NB;
       const int items = tiles * (tiles + 1) / 2;
       tile::Operands o{L21, ld, 1, L21, 1, ld, rest, rest, nb};
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      auto do_item = [&](int it) {
         // it -> (ti, tj) with tj <= ti (row-major over the lower triangle of tiles)
         int ti = (int)((sqrt(8.0 * it + 1.0) - 1.0) / 2.0);
         while ((ti + 1) * (ti + 2) / 2 <= it) ++ti;
@@ -192,24 +240,24 @@ __global__ void __launch_bounds__(NT) chol_fused_kernel(CholArgs a) {
         tile::for_each_acc<CF>(ti * NB, tj * NB, rest, rest, acc, [&](int r, int c, double v) {
           if (c <= r) A22[(long long)r * ld + c] -= v;
         });
+      };
+      if (blockIdx.x == 0) {
+        do_item(0);
+        __threadfence_block();
+        __syncthreads();
+        const int nb2 = min(NB, rest);
+        const int b = factor_diag(A, ld, j0 + nb, nb2, smem);
+        if (threadIdx.x == 0 && b != 0) *a.info = b;
+        if (b == 0) invert_lower(smem, nb2, a.Linv + (long long)(bk + 1) * NB * NB);
       }
+      const int G1 = gridDim.x > 1 ? gridDim.x - 1 : 1;
+      const int me = gridDim.x > 1 ? (int)blockIdx.x - 1 : 0;
+      if (gridDim.x == 1 || blockIdx.x > 0)
+        for (int it = 1 + me; it < items; it += G1) do_item(it);
     }
     grid.sync();
     mark(3);
   }
-
-  // ---- invert every diagonal block (in parallel over CTAs)
-  for (int bk = blockIdx.x; bk < nblk; bk += gridDim.x) {
-    const int j0 = bk * NB, nb = min(NB, dim - j0);
-    for (int e = threadIdx.x; e < NB * NB; e += NT) {
-      const int i = e / NB, j = e % NB;
-      smem[i * LD + j] = (i < nb && j <= i) ? __ldcg(A + (long long)(j0 + i) * ld + j0 + j) : (i == j ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    invert_lower(smem, NB, a.Linv + (long long)bk * NB * NB);
-  }
-  grid.sync();
-  mark(4);
 
   // ---- forward: L y = b.  Every CTA forms y_j = Linv_j x_j itself (x_j is final
   // once the previous blocks' updates are in), then updates its rows below; y goes to

@@ -597,7 +597,7 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
 
 static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   const int m = in.rows, n = in.cols;
-  static const int big_at = std::getenv("QTT_BJ_MIN") ? std::atoi(std::getenv("QTT_BJ_MIN")) : 256;
+  static const int big_at = std::getenv("QTT_BJ_MIN") ? std::atoi(std::getenv("QTT_BJ_MIN")) : 160;
   if (std::min(m, n) >= big_at) {
     svd_block_jacobi(c, in, U, s, Vt);
     return;
