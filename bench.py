@@ -47,6 +47,16 @@ def fp64_peak():
         (40.0, "fallback nominal B200 FP64 tensor")
 
 
+def k1_traffic():
+    """DRAM bytes per K1 call inside the CG kernel, from the committed ncu --set full capture
+    (profiles/r01/cg_tma_traffic.json; the operands stay L2-resident across iterations)."""
+    p = os.path.join(ROOT, "profiles", "r01", "cg_tma_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return {"dram_bytes_per_k1": d["dram_bytes_per_k1"], "shape": d["shape"], "source": d["source"]}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -322,7 +332,7 @@ def run_ours(args, world, rank, local):
                        "avg_us": 1e3 * stats["k1_ms"] / max(1, stats["k1_calls"])},
         "share_of_step": stats["k1_ms"] / 1e3 / max(1e-9, sum(times)),
         "env_update_tflops": stats["env_timed_flops"] / stats["env_ms"] / 1e9 if stats["env_ms"] > 0 else None,
-        "traffic": None,
+        "traffic": k1_traffic(),
     }
     line = {"metric": "time-to-solution at 2^30 cells (C3 QTT AMEn solve)", "value": value, "unit": "s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
