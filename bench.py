@@ -54,7 +54,7 @@ def k1_traffic():
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    return {"dram_bytes_per_k1": d["dram_bytes_per_k1"], "shape": d["shape"], "source": d["source"]}
+    return d["dram_bytes_per_k1"], f"DRAM bytes per K1 call at {d['shape']}, {d['source']}"
 
 
 def dist_setup():
@@ -332,8 +332,11 @@ def run_ours(args, world, rank, local):
                        "avg_us": 1e3 * stats["k1_ms"] / max(1, stats["k1_calls"])},
         "share_of_step": stats["k1_ms"] / 1e3 / max(1e-9, sum(times)),
         "env_update_tflops": stats["env_timed_flops"] / stats["env_ms"] / 1e9 if stats["env_ms"] > 0 else None,
-        "traffic": k1_traffic(),
+        "traffic": None,
     }
+    tr = k1_traffic()
+    if tr is not None:
+        roofline["traffic"], roofline["traffic_source"] = tr
     line = {"metric": "time-to-solution at 2^30 cells (C3 QTT AMEn solve)", "value": value, "unit": "s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
