@@ -135,6 +135,12 @@ int qtt_tt_round(qtt_ctx* ctx, const qtt_train* a, double rel_tol, int max_rank,
                  qtt_train** out);                                            /* tt.py:409, 506 */
 int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x,
                  qtt_train** out);                                            /* tt.py:434 (policy=None) */
+/* Dense bridges (tt.py:276-298).  qtt_tt_entries: count entries at multi-indices idx
+ * (host int32, count x order, row-major) -> out (host, count doubles); the product of core
+ * slices left to right, as tt_entry.  qtt_tt_to_dense: the full C-order (big-endian mode)
+ * vector, prod(dims) doubles -> out (host); the reference caps it at 2^22 entries. */
+int qtt_tt_entries(qtt_ctx* ctx, const qtt_train* t, const int32_t* idx, int64_t count, double* out); /* tt.py:286 */
+int qtt_tt_to_dense(qtt_ctx* ctx, const qtt_train* t, int64_t total, double* out);                    /* tt.py:276 */
 /* Config-4 microbench: right-environment pre-pass (amen.py:300-321,
  * _phi_right_step amen.py:114 with bra = ket = x), then one left-to-right sweep of
  * _local_matvec(phi_L[k], A_k, phi_R[k+1], x_k) (amen.py:134) and

@@ -76,6 +76,8 @@ SIGNATURES = {
     "qtt_tt_dot": [_VP, _VP, _VP, _P],
     "qtt_tt_round": [_VP, _VP, ctypes.c_double, _I, ctypes.POINTER(_VP)],
     "qtt_tt_apply": [_VP, _VP, _VP, ctypes.POINTER(_VP)],
+    "qtt_tt_entries": [_VP, _VP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _P],
+    "qtt_tt_to_dense": [_VP, _VP, ctypes.c_int64, _P],
     "qtt_matvec_sweep": [_VP, _VP, _VP, _I, ctypes.POINTER(_VP), _P],
     "qtt_residual_norm": [_VP, _VP, _VP, _VP, _I, _P, ctypes.POINTER(_I)],
     "qtt_qr": [_VP, _P, _I, _I, _P, _P],

@@ -260,6 +260,42 @@ int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train
   });
 }
 
+int qtt_tt_entries(qtt_ctx* ctx, const qtt_train* t, const int32_t* idx, int64_t count, double* out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& tt = T(t);
+    if (count < 0) throw qtt::Error(QTT_ERR_ARG, "negative count");
+    const int K = tt.order();
+    for (int64_t e = 0; e < count; ++e)
+      for (int k = 0; k < K; ++k) {
+        const int n = tt.cores[k].m * tt.cores[k].n;
+        if (idx[e * K + k] < 0 || idx[e * K + k] >= n)
+          throw qtt::Error(QTT_ERR_ARG, "digit " + std::to_string(idx[e * K + k]) + " out of range at mode " +
+                                            std::to_string(k));
+      }
+    if (count == 0) return;
+    qtt::DBuf di(qtt::cdiv(count * K, 2) + 1, c.stream), dout(count, c.stream);
+    QTT_CUDA(cudaMemcpyAsync(di.p, idx, (size_t)count * K * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+    qtt::tt_entries(c, tt, reinterpret_cast<const int*>(di.p), count, dout.p);
+    dout.download(out, count);
+    c.sync();
+  });
+}
+
+int qtt_tt_to_dense(qtt_ctx* ctx, const qtt_train* t, int64_t total, double* out) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    const qtt::Train& tt = T(t);
+    long long prod = 1;
+    for (const auto& k : tt.cores) prod *= (long long)k.m * k.n;
+    if (prod != total) throw qtt::Error(QTT_ERR_SHAPE, "output size does not match prod(dims)");
+    qtt::DBuf d(total, c.stream);
+    qtt::tt_full(c, tt, d.p);
+    d.download(out, total);
+    c.sync();
+  });
+}
+
 int qtt_matvec_sweep(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, int split_timing,
                      qtt_train** y_out, double* times) {
   return guarded([&] {

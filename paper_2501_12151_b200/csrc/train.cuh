@@ -71,6 +71,11 @@ double residual_norm_exact(Ctx& c, const Train& A, const Train& x, const Train& 
 // Diagnostic Gram estimate (fast, loses digits when ||A|| ||x|| >> ||Ax - f||).
 double residual_norm_gram(Ctx& c, const Train& A, const Train& x, const Train& f);
 
+// Dense bridges (tt.py:276-298): entries at count multi-indices (device int array, count x K,
+// row-major) into out_dev; the full C-order vector (prod dims doubles) into out_dev.
+void tt_entries(Ctx& c, const Train& t, const int* idx_dev, long long count, double* out_dev);
+void tt_full(Ctx& c, const Train& t, double* out_dev);
+
 // Rank rule of tt.py:386-393, bit-for-bit given the same singular values.
 int rank_for_tolerance(const double* s, int n, double delta);
 

@@ -571,4 +571,95 @@ double residual_norm(Ctx& c, const Train& A, const Train& x, const Train& f, boo
   return residual_norm_exact(c, A, x, f);
 }
 
+// ---------------------------------------------------------------- dense bridges (tt.py:276-298)
+namespace {
+struct CoreRef {
+  const double* p;
+  int r0, n, r1;
+};
+
+// One CTA per requested entry: v <- v . core_k[:, idx_k, :] left to right (tt.py:288-298);
+// v lives in shared memory, threads walk the right rank (coalesced core rows).
+__global__ void tt_entries_kernel(const CoreRef* cores, int K, const int* idx, long long count, double* out,
+                                  int maxr) {
+  extern __shared__ double sv[];
+  double* v = sv;
+  double* w = sv + maxr;
+  for (long long e = blockIdx.x; e < count; e += gridDim.x) {
+    const int* id = idx + e * K;
+    __syncthreads();
+    if (threadIdx.x == 0) v[0] = 1.0;
+    __syncthreads();
+    int rl = 1;
+    for (int k = 0; k < K; ++k) {
+      const CoreRef c = cores[k];
+      const int d = id[k];
+      for (int j = threadIdx.x; j < c.r1; j += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < rl; ++i) s = fma(v[i], __ldg(c.p + ((long long)i * c.n + d) * c.r1 + j), s);
+        w[j] = s;
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < c.r1; j += blockDim.x) v[j] = w[j];
+      __syncthreads();
+      rl = c.r1;
+    }
+    if (threadIdx.x == 0) out[e] = v[0];
+  }
+}
+}  // namespace
+
+void tt_entries(Ctx& c, const Train& t, const int* idx_dev, long long count, double* out_dev) {
+  const int K = t.order();
+  std::vector<CoreRef> h(K);
+  int maxr = 1;
+  for (int k = 0; k < K; ++k) {
+    const Core& ck = t.cores[k];
+    h[k] = CoreRef{ck.d.p, ck.r0, ck.m * ck.n, ck.r1};
+    maxr = std::max(maxr, std::max(ck.r0, ck.r1));
+  }
+  DBuf tab((long long)cdiv((long long)K * sizeof(CoreRef), 8), c.stream);
+  QTT_CUDA(cudaMemcpyAsync(tab.p, h.data(), K * sizeof(CoreRef), cudaMemcpyHostToDevice, c.stream));
+  const size_t sh = 2 * (size_t)maxr * sizeof(double);
+  if (sh > 200 * 1024) throw Error(QTT_ERR_CAPACITY, "tt_entry: rank too large for the shared-memory kernel");
+  if (sh > 48 * 1024)
+    QTT_CUDA(cudaFuncSetAttribute(tt_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+  const int grid = (int)std::min<long long>(count, 148LL * 16);
+  if (grid > 0) {
+    tt_entries_kernel<<<grid, 128, sh, c.stream>>>(reinterpret_cast<const CoreRef*>(tab.p), K, idx_dev, count,
+                                                   out_dev, maxr);
+    QTT_CHECK_LAUNCH();
+  }
+  c.sync();  // the host core table must outlive the copy
+}
+
+// Full contraction (tt.py:276-283): v (P x r) <- v . core (r x n r'), P grows by n per core.
+void tt_full(Ctx& c, const Train& t, double* out_dev) {
+  const int K = t.order();
+  long long P = 1;
+  DBuf a(1, c.stream), b;
+  fill(c, a.p, 1, 1.0);
+  int r = 1;
+  for (int k = 0; k < K; ++k) {
+    const Core& ck = t.cores[k];
+    const int nn = ck.m * ck.n;
+    const long long cols = (long long)nn * ck.r1;
+    double* dst = (k == K - 1) ? out_dev : nullptr;
+    if (!dst) {
+      b.alloc(P * cols, c.stream);
+      dst = b.p;
+    }
+    GemmArgs g;
+    g.M = (int)P; g.N = (int)cols; g.K = r;
+    gemm_set_A(g, a.p, r, false);
+    gemm_set_B(g, ck.d.p, cols, false);
+    gemm_set_C(g, dst, cols);
+    DBuf ws(gemm_workspace_hint(g) + 1, c.stream);
+    gemm(g, c.stream, ws.p, ws.n);
+    P *= nn;
+    r = ck.r1;
+    if (k != K - 1) std::swap(a, b);
+  }
+}
+
 }  // namespace qtt

@@ -240,3 +240,23 @@ def test_residual_norm_structured_sweep_vs_oracle(L, r):
     ref = O.residual_norm(prob.op, x, prob.rhs)
     got = residual_norm(TTLinearOperator(prob.op), TensorTrain(x), TensorTrain(prob.rhs))
     assert abs(got - ref) <= 1e-11 * ref
+
+
+def test_dense_bridges_vs_oracle(tt):
+    """tt_to_dense (GEMM chain) and batched tt_entry on the device against the oracle's
+    contraction (tt.py:276-298), including the leading 3-component mode."""
+    rng = np.random.default_rng(11)
+    dims = (3, 2, 2, 2, 2, 2, 2, 2)
+    ranks = [1, 3, 5, 7, 6, 4, 5, 2, 1]
+    cores = [rng.standard_normal((ranks[k], dims[k], ranks[k + 1])) for k in range(len(dims))]
+    t = tt.TensorTrain(cores)
+    full = tt.tt_to_dense(t)
+    ref = O.tt_full(cores)
+    assert rel(full, ref) <= 1e-14
+    idx = np.stack([rng.integers(0, d, size=50) for d in dims], axis=1)
+    got = tt.tt_entries(t, idx)
+    flat = np.ravel_multi_index(tuple(idx.T), dims)
+    assert np.max(np.abs(got - ref[flat])) <= 1e-13 * np.max(np.abs(ref))
+    assert abs(tt.tt_entry(t, list(idx[0])) - ref[flat[0]]) <= 1e-13 * np.max(np.abs(ref))
+    with pytest.raises(ValueError):
+        tt.tt_entry(t, [3] + [0] * (len(dims) - 1))
