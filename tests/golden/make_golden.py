@@ -307,7 +307,25 @@ def qtt1_cases():
     rser.save_tt(a, os.path.join(HERE, "op.qtt1"))
 
 
+def op_round_cases():
+    """tt_op_round (tt.py:506-531) of an operator whose ranks double (A + A, A = the L=2 cube
+    stiffness of this repo's assembly) and of a random operator, as the reference computes it."""
+    d = {}
+    A = rtt.TTLinearOperator(assemble_cube(2).op)
+    AA = rtt.tt_op_add(A, A)
+    put_train(d, "AA", list(AA.cores))
+    put_train(d, "AA_round", list(rtt.tt_op_round(AA, rtt.TruncationPolicy(1e-10)).cores))
+    rng = np.random.default_rng(21)
+    B = rtt.TTLinearOperator(rand_op(rng, (2, 2, 2, 2, 2), [4, 6, 6, 4], 0.5))
+    put_train(d, "B", list(B.cores))
+    put_train(d, "B_round", list(rtt.tt_op_round(B, rtt.TruncationPolicy(1e-2, 3)).cores))
+    np.savez_compressed(os.path.join(HERE, "op_round.npz"), **d)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "opround":
+        op_round_cases()
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "qtt1":
         qtt1_cases()
         return
@@ -316,6 +334,7 @@ def main():
         return
     np.savez_compressed(os.path.join(HERE, "c4_small.npz"), **c4_cases())
     qtt1_cases()
+    op_round_cases()
     np.savez_compressed(os.path.join(HERE, "kernels_bin.npz"), **kernels_case(1, (2,) * 8, 12, 6, 4))
     np.savez_compressed(os.path.join(HERE, "kernels_lead3.npz"), **kernels_case(2, (3,) + (2,) * 7, 10, 7, 4))
     np.savez_compressed(os.path.join(HERE, "factor.npz"), **factor_cases())

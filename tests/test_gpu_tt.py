@@ -260,3 +260,14 @@ def test_dense_bridges_vs_oracle(tt):
     assert abs(tt.tt_entry(t, list(idx[0])) - ref[flat[0]]) <= 1e-13 * np.max(np.abs(ref))
     with pytest.raises(ValueError):
         tt.tt_entry(t, [3] + [0] * (len(dims) - 1))
+
+
+def test_op_round_vs_reference(tt):
+    """tt_op_round over fused (row, col) modes (tt.py:506-531): ranks and dense operator equal
+    to the reference's, for a rank-doubled stiffness (A + A) and a capped random operator."""
+    d = load("op_round.npz")
+    for name, pol in (("AA", tt.TruncationPolicy(1e-10)), ("B", tt.TruncationPolicy(1e-2, 3))):
+        out = tt.tt_op_round(tt.TTLinearOperator(train(d, name)), pol)
+        ref = train(d, f"{name}_round")
+        assert [c.shape for c in out.cores] == [c.shape for c in ref], name
+        assert rel(O.op_full(list(out.cores)), O.op_full(ref)) <= 1e-12, name

@@ -116,3 +116,16 @@ def test_amen_trajectory(case):
     x0 = train(d, "x0") if "x0__n" in d else None
     x, rep = O.amen_solve(train(d, "A"), train(d, "f"), x0, amen_config(d))
     check_amen_parity(d, rep, O.tt_full(x))
+
+
+def test_op_round_oracle_vs_reference():
+    """The oracle's tt_round over fused (m*n) modes reproduces the reference's tt_op_round."""
+    d = load("op_round.npz")
+    for name, (tol, cap) in (("AA", (1e-10, None)), ("B", (1e-2, 3))):
+        A = train(d, name)
+        fused = [c.reshape(c.shape[0], c.shape[1] * c.shape[2], c.shape[3]) for c in A]
+        out = O.tt_round(fused, tol, cap)
+        ref = train(d, f"{name}_round")
+        assert [c.shape[0] for c in out] == [c.shape[0] for c in ref]
+        outc = [c.reshape(r.shape) for c, r in zip(out, ref)]
+        assert rel(O.op_full(outc), O.op_full(ref)) <= 1e-12
