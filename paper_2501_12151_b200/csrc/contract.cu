@@ -23,11 +23,28 @@ __global__ void permute_op_core_kernel(const double* __restrict__ A, int R0, int
   }
 }
 
+__global__ void transpose_rows_kernel(const double* __restrict__ in, double* __restrict__ out, long long rows,
+                                      long long cols, long long ldo) {
+  __shared__ double tile[32][33];
+  const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const long long r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const long long c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][i];
+  }
+}
+
 // split-K workspace a plain M x N x K product may ask for (gemm.cu plan)
 long long splitk_ws(int M, int N, int K) {
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
-  return gemm_workspace_hint(g);
+  GemmArgs t = g;  // the same product with K-contiguous operands may take the TMA path
+  t.a_rs = K; t.a_cs = 1; t.b_rs = 1; t.b_cs = K + (K & 1); t.c_rs = N; t.c_cs = 1;
+  return std::max(gemm_workspace_hint(g), gemm_workspace_hint(t));
 }
 
 inline Scratch take(Scratch& sc, long long n) {
@@ -39,6 +56,13 @@ inline Scratch take(Scratch& sc, long long n) {
 }
 
 }  // namespace
+
+// out[c][r] = in[r][c] (in: rows x cols row-major; out rows = cols, pitch ldo)
+void transpose_rows(const double* in, double* out, long long rows, long long cols, long long ldo, cudaStream_t s) {
+  dim3 g((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32));
+  transpose_rows_kernel<<<g, dim3(32, 8), 0, s>>>(in, out, rows, cols, ldo);
+  QTT_CHECK_LAUNCH();
+}
 
 void permute_op_core(const double* A, int R0, int m, int n, int R1, double* Ap, double* Aq,
                      cudaStream_t s) {
@@ -132,8 +156,14 @@ void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int
 }
 
 // ---------------------------------------------------------------- local matvec
+// Step 1 reads v as B^T (K = U contiguous) when the product is large enough for the TMA
+// GEMM path: v is transposed into scratch first (rU x n*rV doubles, cheap next to the GEMM).
+static bool step1_transposed(int rX, int Ra, int rU, int n, int rV) {
+  return (double)rX * Ra * n * rV * rU >= (double)(1 << 24) && rU >= 64 && rX * Ra >= 64 && n * rV >= 32;
+}
+
 long long local_matvec_scratch(int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV) {
-  return (long long)rX * Ra * n * rV + (long long)rX * m * Rb * rV +
+  return (long long)rX * Ra * n * rV + (long long)rX * m * Rb * rV + (long long)(rU + 1) * n * rV +
          std::max(splitk_ws(rX * Ra, n * rV, rU), splitk_ws(rX * m, rY, Rb * rV));
 }
 
@@ -146,7 +176,14 @@ void local_matvec(const double* phil, int rX, int Ra, int rU, const double* Ap, 
     GemmArgs g;
     g.M = rX * Ra; g.N = n * rV; g.K = rU;
     gemm_set_A(g, phil, rU, false);
-    gemm_set_B(g, v, (long long)n * rV, false);
+    if (skip == nullptr && step1_transposed(rX, Ra, rU, n, rV)) {
+      const long long ldt = rU + (rU & 1);  // 16-byte row pitch for the tensor map
+      double* vT = take(sc, ldt * n * rV).p;  // [(n,V)][U]
+      transpose_rows(v, vT, rU, (long long)n * rV, ldt, s);
+      g.B = vT; g.b_rs = 1; g.b_cs = ldt;
+    } else {
+      gemm_set_B(g, v, (long long)n * rV, false);
+    }
     gemm_set_C(g, t1, (long long)n * rV);
     g.skip = skip;
     gemm(g, s, sc.p, sc.n);

@@ -61,6 +61,9 @@ void local_dense(const double* phil, int rX, int Ra, int rU, const double* A, in
 void local_diag(const double* phil, int rX, int Ra, const double* A, int m, int Rb, const double* phir,
                 int rY, double* out, Scratch sc, cudaStream_t s);
 
+// out[c][r] = in[r][c]  (in: rows x cols row-major; out: cols rows with pitch ldo)
+void transpose_rows(const double* in, double* out, long long rows, long long cols, long long ldo, cudaStream_t s);
+
 // Flop counts (algorithmic), for the roofline.
 double local_matvec_flops(int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV);
 double env_flops(int rX, int RA, int rY, int m, int n, int RB, int rU, int rZ);

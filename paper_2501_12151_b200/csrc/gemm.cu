@@ -6,6 +6,7 @@
 
 #include "dmma_tile.cuh"
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
 
 namespace qtt {
 namespace {
@@ -133,7 +134,13 @@ Plan plan_for(const GemmArgs& g) {
 
 }  // namespace
 
+static bool tma_path_on() {
+  static const bool on = !(std::getenv("QTT_GEMM_TMA") && std::atoi(std::getenv("QTT_GEMM_TMA")) == 0);
+  return on;
+}
+
 long long gemm_workspace_hint(const GemmArgs& g) {
+  if (tma_path_on() && gemm_tma_eligible(g)) return gemm_tma_workspace(g);
   Plan p = plan_for(g);
   return p.splits > 1 ? (long long)p.splits * g.M * g.N : 0;
 }
@@ -151,6 +158,7 @@ void gemm(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_doubles) {
       }
     return;
   }
+  if (tma_path_on() && gemm_tma(g, s, ws, ws_doubles)) return;
   Plan p = plan_for(g);
   if (g.lower_only) {
     p.splits = 1;

@@ -24,7 +24,7 @@ int main() {
     GemmArgs g;
     g.M = s.M; g.N = s.N; g.K = s.K;
     gemm_set_A(g, A.p, s.K, false);
-    gemm_set_B(g, B.p, s.N, false);
+    gemm_set_B(g, B.p, s.K, true);  // B stored [N][K]: K-contiguous operands (TMA-eligible)
     gemm_set_C(g, C.p, s.N);
     DBuf ws(gemm_workspace_hint(g) + 1, c.stream);
     for (int w = 0; w < 3; ++w) gemm(g, c.stream, ws.p, ws.n);

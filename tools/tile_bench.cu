@@ -166,7 +166,7 @@ template <int NF, bool DD>
 __global__ void __launch_bounds__(384, 1) bench_fb_kernel(const __grid_constant__ TmaMaps maps, double* C, int M,
                                                            int N, int K, int items, int rb, int cb, int stride) {
   extern __shared__ unsigned char smem_raw[];
-  tmafb::Ring ring = tmafb::ring_init(smem_raw, stride);
+  tmafb::Ring ring = tmafb::ring_init(smem_raw, stride, tmafb::STAGES);
   const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int nrb = (FR + rb - 1) / rb, ncb = (FC + cb - 1) / cb;
   const int KT = (K + 15) / 16;
