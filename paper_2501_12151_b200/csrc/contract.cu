@@ -72,9 +72,15 @@ void permute_op_core(const double* A, int R0, int m, int n, int R1, double* Ap, 
   QTT_CHECK_LAUNCH();
 }
 
+// Step 1 reads v as B^T (K = U contiguous) when the product is large enough for the TMA
+// GEMM path: v is transposed into scratch first (rU x n*rV doubles, cheap next to the GEMM).
+static bool step1_transposed(int rX, int Ra, int rU, int n, int rV) {
+  return (double)rX * Ra * n * rV * rU >= (double)(1 << 24) && rU >= 64 && rX * Ra >= 64 && n * rV >= 32;
+}
+
 // ---------------------------------------------------------------- left environment
 long long env_left_scratch(int rX, int RA, int rY, int m, int n, int RB, int rZ, int rU) {
-  return (long long)rX * RA * n * rZ + (long long)rX * m * RB * rZ +
+  return (long long)rX * RA * n * rZ + (long long)rX * m * RB * rZ + (long long)(rY + 1) * n * rZ +
          std::max(splitk_ws(rX * RA, n * rZ, rY), splitk_ws(rU, RB * rZ, rX * m));
 }
 
@@ -83,11 +89,18 @@ void env_left(const double* phi, int rX, int RA, int rY, const double* bra, int 
               Scratch sc, cudaStream_t s) {
   double* t1 = take(sc, (long long)rX * RA * n * rZ).p;  // [X][A][n][Z]
   double* t2 = take(sc, (long long)rX * m * RB * rZ).p;  // [X][m][B][Z]
-  {  // t1[(X,A),(n,Z)] = phi[(X,A),Y] @ ket[Y,(n,Z)]
+  {  // t1[(X,A),(n,Z)] = phi[(X,A),Y] @ ket[Y,(n,Z)]   (ket read transposed when large: TMA path)
     GemmArgs g;
     g.M = rX * RA; g.N = n * rZ; g.K = rY;
     gemm_set_A(g, phi, rY, false);
-    gemm_set_B(g, ket, (long long)n * rZ, false);
+    if (step1_transposed(rX, RA, rY, n, rZ)) {
+      const long long ldt = rY + (rY & 1);
+      double* kT = take(sc, ldt * n * rZ).p;  // [(n,Z)][Y]
+      transpose_rows(ket, kT, rY, (long long)n * rZ, ldt, s);
+      g.B = kT; g.b_rs = 1; g.b_cs = ldt;
+    } else {
+      gemm_set_B(g, ket, (long long)n * rZ, false);
+    }
     gemm_set_C(g, t1, (long long)n * rZ);
     gemm(g, s, sc.p, sc.n);
   }
@@ -156,12 +169,6 @@ void env_right(const double* phi, int rX, int RA, int rZ, const double* bra, int
 }
 
 // ---------------------------------------------------------------- local matvec
-// Step 1 reads v as B^T (K = U contiguous) when the product is large enough for the TMA
-// GEMM path: v is transposed into scratch first (rU x n*rV doubles, cheap next to the GEMM).
-static bool step1_transposed(int rX, int Ra, int rU, int n, int rV) {
-  return (double)rX * Ra * n * rV * rU >= (double)(1 << 24) && rU >= 64 && rX * Ra >= 64 && n * rV >= 32;
-}
-
 long long local_matvec_scratch(int rX, int Ra, int rU, int m, int n, int Rb, int rY, int rV) {
   return (long long)rX * Ra * n * rV + (long long)rX * m * Rb * rV + (long long)(rU + 1) * n * rV +
          std::max(splitk_ws(rX * Ra, n * rV, rU), splitk_ws(rX * m, rY, Rb * rV));
