@@ -273,7 +273,10 @@ def run_ours(args, world, rank, local):
         return amen_solve_device(dA, df, dx0, cfg, draws, K, ctx)
 
     for _ in range(args.warmup):
-        solve_resident()
+        _, winfo = solve_resident()
+        if os.environ.get("BENCH_VERBOSE"):
+            print(f"warmup solve: {winfo['sweeps_used']} sweeps, {winfo['final_relative_residual']!r}",
+                  file=sys.stderr, flush=True)
     ctx.synchronize()
 
     ctx.set_profiling(True)  # deferred CUDA events around every K1/K2 launch (no syncs)
