@@ -90,3 +90,21 @@ def test_config_c1_vs_reference_ensemble():
     assert max(x.ranks) == max(ref["ranks"])
     slo, shi = ref["band_sweeps"]
     assert slo <= rep.sweeps_used <= shi
+
+
+def test_solve_is_bitwise_reproducible():
+    """Two solves of the same rank-limited system (C1 settings at L = 3, 8 sweeps) give
+    bitwise identical residual histories and solutions: every reduction (split-K, CG dot
+    products, Gershgorin max) has a fixed order, so trajectory differences can only come
+    from different inputs or builds."""
+    from paper_2501_12151_b200.amen import AmenConfig, amen_solve
+    from paper_2501_12151_b200.assembly3d import assemble_cube
+    from paper_2501_12151_b200.configs import x0_rank2
+    from paper_2501_12151_b200.tt import TensorTrain, TruncationPolicy, TTLinearOperator
+    prob = assemble_cube(3)
+    cfg = AmenConfig(residual_tol=1e-6, max_sweeps=8, rounding=TruncationPolicy(1e-6, 16), seed=2024)
+    runs = [amen_solve(TTLinearOperator(prob.op), TensorTrain(prob.rhs), TensorTrain(x0_rank2(prob.dims)), cfg)
+            for _ in range(2)]
+    (x1, r1), (x2, r2) = runs
+    assert r1.residual_history == r2.residual_history
+    assert all(np.array_equal(a, b) for a, b in zip(x1.cores, x2.cores))
