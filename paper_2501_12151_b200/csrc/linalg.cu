@@ -471,18 +471,17 @@ __global__ void __launch_bounds__(256) kron_core_kernel(const double* __restrict
     }
     double* yr = y + row * cols;
     if ((rx1 & 1) == 0 && (cols & 1) == 0) {  // pairs of yy: 16-byte streaming stores, no division
-      const int h = rx1 >> 1;
-      for (int b = 0; b < Ra1; ++b) {
-        double2* dst = reinterpret_cast<double2*>(yr + (long long)b * rx1);
-        for (int j = threadIdx.x; j < h; j += blockDim.x) {
-          double s0 = 0.0, s1 = 0.0;
-          for (int nn = 0; nn < n; ++nn) {
-            const double av = sa[nn * Ra1 + b];
-            s0 = fma(av, sx[nn * rx1 + 2 * j], s0);
-            s1 = fma(av, sx[nn * rx1 + 2 * j + 1], s1);
-          }
-          __stcs(dst + j, make_double2(s0, s1));
+      const int h = rx1 >> 1;  // (b, j) pairs flattened: every thread busy even when rx1 < 2 * blockDim
+      double2* dst = reinterpret_cast<double2*>(yr);
+      for (int e = threadIdx.x; e < Ra1 * h; e += blockDim.x) {
+        const int b = e / h, j = e - b * h;
+        double s0 = 0.0, s1 = 0.0;
+        for (int nn = 0; nn < n; ++nn) {
+          const double av = sa[nn * Ra1 + b];
+          s0 = fma(av, sx[nn * rx1 + 2 * j], s0);
+          s1 = fma(av, sx[nn * rx1 + 2 * j + 1], s1);
         }
+        __stcs(dst + e, make_double2(s0, s1));
       }
     } else {
       for (int e = threadIdx.x; e < cols; e += blockDim.x) {
