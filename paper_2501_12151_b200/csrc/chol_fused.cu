@@ -157,7 +157,7 @@ __device__ void invert_lower(const double* s, int nb, double* Linv) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT) chol_fused_kernel(CholArgs a) {
+__global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs a) {
   extern __shared__ double smem[];
   __shared__ double yb[NB];
   cg::grid_group grid = cg::this_grid();
@@ -259,51 +259,124 @@ __global__ void __launch_bounds__(NT) chol_fused_kernel(CholArgs a) {
     mark(3);
   }
 
-  // ---- forward: L y = b.  Every CTA forms y_j = Linv_j x_j itself (x_j is final
-  // once the previous blocks' updates are in), then updates its rows below; y goes to
-  // a separate buffer so no CTA overwrites an x_j another CTA is still reading.
+  // ---- triangular solves in groups of GS = 4 diagonal blocks per grid barrier: every CTA
+  // solves the group's 256 x 256 diagonal part itself (block by block with the inverted
+  // 64 x 64 blocks and the in-group off-diagonal blocks; redundant but tiny), then updates
+  // its share of the rows outside the group -- 16 barriers per direction at dim 4096
+  // instead of 64.  y goes to a separate buffer so no CTA overwrites an x another still reads.
+  constexpr int GS = 4;
+  __shared__ double xg[GS * NB];
   double* x = a.x;
   double* y = a.y;
-  for (int bk = 0; bk < nblk; ++bk) {
-    const int j0 = bk * NB, nb = min(NB, dim - j0);
-    const double* Li = a.Linv + (long long)bk * NB * NB;
-    if (warp < 2) {  // 64 rows of the 64x64 product, one row per thread of warps 0-1
-      const int i = threadIdx.x;
-      double s = 0.0;
-      for (int j = 0; j <= i && j < nb; ++j) s += __ldcg(Li + i * NB + j) * __ldcg(x + j0 + j);
-      yb[i] = i < nb ? s : 0.0;
-    }
+  // forward: L y = b
+  for (int bk0 = 0; bk0 < nblk; bk0 += GS) {
+    const int g0 = bk0 * NB;
+    const int grows = min(GS * NB, dim - g0);
+    for (int i = threadIdx.x; i < grows; i += NT) xg[i] = __ldcg(x + g0 + i);
     __syncthreads();
+    for (int g = 0; g < GS && bk0 + g < nblk; ++g) {
+      const int bk = bk0 + g, j0 = bk * NB, nb = min(NB, dim - j0);
+      const double* Li = a.Linv + (long long)bk * NB * NB;
+      {  // y_g = Linv_g x_g: 4 lanes per row, 16 independent loads in flight per lane
+        const int i = threadIdx.x >> 2, part = threadIdx.x & 3;
+        double lv[NB / 4];
+#pragma unroll
+        for (int k = 0; k < NB / 4; ++k) {
+          const int jj = part + 4 * k;
+          lv[k] = (jj <= i && jj < nb) ? __ldcg(Li + i * NB + jj) : 0.0;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB / 4; ++k) s = fma(lv[k], xg[g * NB + part + 4 * k], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (part == 0) yb[i] = i < nb ? s : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nb; i += NT) xg[g * NB + i] = yb[i];  // xg now holds y_g
+      // in-group rows below: x[r] -= L[r, block g] y_g   (one warp per row)
+      for (int r = j0 + nb + warp; r < g0 + grows; r += NT / 32) {
+        double t = 0.0;
+        for (int jj = lane; jj < nb; jj += 32) t = fma(A[(long long)r * ld + j0 + jj], yb[jj], t);
+        t = warp_sum(t);
+        if (lane == 0) xg[r - g0] -= t;
+      }
+      __syncthreads();
+    }
     if (blockIdx.x == 0)
-      for (int i = threadIdx.x; i < nb; i += NT) y[j0 + i] = yb[i];
-    for (int row = j0 + nb + gwarp; row < dim; row += nwarps) {  // one warp per row
-      double s = 0.0;
-      for (int j = lane; j < nb; j += 32) s += A[(long long)row * ld + j0 + j] * yb[j];
-      s = warp_sum(s);
-      if (lane == 0) x[row] -= s;
+      for (int i = threadIdx.x; i < grows; i += NT) y[g0 + i] = xg[i];
+    // rows below the group: x[row] -= L[row, group] y_group   (one warp per row)
+    for (int row = g0 + grows + gwarp; row < dim; row += nwarps) {
+      double av[GS * NB / 32];
+#pragma unroll
+      for (int k = 0; k < GS * NB / 32; ++k) {
+        const int jj = lane + 32 * k;
+        av[k] = jj < grows ? A[(long long)row * ld + g0 + jj] : 0.0;
+      }
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < GS * NB / 32; ++k) t = fma(av[k], lane + 32 * k < grows ? xg[lane + 32 * k] : 0.0, t);
+      t = warp_sum(t);
+      if (lane == 0) x[row] -= t;
     }
     grid.sync();
   }
   mark(5);
-  // ---- backward: L^T u = y, blocks last to first: u_j = Linv_j^T y_j (y is the
-  // working vector, updated above the block; u is written to x)
-  for (int bk = nblk - 1; bk >= 0; --bk) {
-    const int j0 = bk * NB, nb = min(NB, dim - j0);
-    const double* Li = a.Linv + (long long)bk * NB * NB;
-    if (warp < 2) {
-      const int i = threadIdx.x;
-      double s = 0.0;
-      for (int j = i; j < nb; ++j) s += __ldcg(Li + j * NB + i) * __ldcg(y + j0 + j);  // (Linv^T)[i][j]
-      yb[i] = i < nb ? s : 0.0;
-    }
+  // backward: L^T u = y, groups last to first (y is the working vector; u is written to x)
+  const int ngrp = (nblk + GS - 1) / GS;
+  for (int gi = ngrp - 1; gi >= 0; --gi) {
+    const int bk0 = gi * GS, g0 = bk0 * NB;
+    const int grows = min(GS * NB, dim - g0);
+    const int nbg = min(GS, nblk - bk0);
+    for (int i = threadIdx.x; i < grows; i += NT) xg[i] = __ldcg(y + g0 + i);
     __syncthreads();
+    for (int g = nbg - 1; g >= 0; --g) {
+      const int bk = bk0 + g, j0 = bk * NB, nb = min(NB, dim - j0);
+      const double* Li = a.Linv + (long long)bk * NB * NB;
+      {  // u_g = Linv_g^T y_g: 4 lanes per row, 16 independent loads in flight per lane
+        const int i = threadIdx.x >> 2, part = threadIdx.x & 3;
+        double lv[NB / 4];
+#pragma unroll
+        for (int k = 0; k < NB / 4; ++k) {
+          const int jj = part + 4 * k;
+          lv[k] = (jj >= i && jj < nb) ? __ldcg(Li + jj * NB + i) : 0.0;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB / 4; ++k) s = fma(lv[k], xg[g * NB + part + 4 * k], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (part == 0) yb[i] = i < nb ? s : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nb; i += NT) xg[g * NB + i] = yb[i];  // xg now holds u_g
+      // in-group columns above: y[c] -= sum_j L[j0 + j, c] u_g[j]   for g0 <= c < j0
+      for (int cidx = g0 + threadIdx.x; cidx < j0; cidx += NT) {
+        double t = 0.0;
+        for (int j16 = 0; j16 < nb; j16 += 16) {
+          double av[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) av[k] = j16 + k < nb ? A[(long long)(j0 + j16 + k) * ld + cidx] : 0.0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) t = fma(av[k], j16 + k < nb ? yb[j16 + k] : 0.0, t);
+        }
+        xg[cidx - g0] -= t;
+      }
+      __syncthreads();
+    }
     if (blockIdx.x == 0)
-      for (int i = threadIdx.x; i < nb; i += NT) x[j0 + i] = yb[i];
-    // y[i] -= sum_j L[j0+j, i] u[j] for i < j0 (coalesced over i)
-    for (int i = blockIdx.x * NT + threadIdx.x; i < j0; i += gridDim.x * NT) {
-      double s = 0.0;
-      for (int j = 0; j < nb; ++j) s += A[(long long)(j0 + j) * ld + i] * yb[j];
-      y[i] -= s;
+      for (int i = threadIdx.x; i < grows; i += NT) x[g0 + i] = xg[i];
+    // rows above the group: y[i] -= sum_{j in group} L[j, i] u[j]  (coalesced over i)
+    for (int i = blockIdx.x * NT + threadIdx.x; i < g0; i += gridDim.x * NT) {
+      double t = 0.0;
+      for (int j16 = 0; j16 < grows; j16 += 16) {
+        double av[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) av[k] = j16 + k < grows ? A[(long long)(g0 + j16 + k) * ld + i] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t = fma(av[k], j16 + k < grows ? xg[j16 + k] : 0.0, t);
+      }
+      y[i] -= t;
     }
     grid.sync();
   }

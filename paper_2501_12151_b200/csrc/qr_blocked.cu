@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "contract.cuh"
 #include "gemm.cuh"
 #include "linalg.cuh"
 #include "qr_blocked.cuh"
@@ -920,6 +921,49 @@ void apply_wy_left(Ctx& c, const double* V, int mrows, int jb, const double* T, 
   }
 }
 
+// The outer compact-WY update in the transposed orientation, so both big products read
+// K-contiguous operands and take the TMA GEMM path (gemm_tma.cu):
+//   Y1^T = C^T V            (n2 x jb;  A = C^T = C's column-major storage, B = V^T stored [jb][mrows])
+//   Y2^T = Y1^T T           (small)
+//   C^T -= Y2^T V^T         (A = Y2^T [n2][jb], B = VT [mrows][jb], the row-major copy of V)
+// C is column-major (ld), i.e. C^T row-major with leading dimension ld: same storage, no copy.
+void apply_wy_left_t(Ctx& c, const double* V, int mrows, int jb, const double* T, long long ldt, double* C,
+                     long long ld, int n2, DBuf& Y1, DBuf& Y2, DBuf& Wsk, DBuf& VT) {
+  if (Y1.n < (long long)jb * n2) Y1.alloc((long long)jb * n2, c.stream);
+  if (Y2.n < (long long)jb * n2) Y2.alloc((long long)jb * n2, c.stream);
+  if (VT.n < (long long)mrows * jb) VT.alloc((long long)mrows * jb, c.stream);
+  transpose_rows(V, VT.p, jb, mrows, jb, c.stream);  // V as [jb][mrows] -> VT [mrows][jb]
+  {  // Y1T [n2][jb] = C^T V
+    GemmArgs g;
+    g.M = n2; g.N = jb; g.K = mrows;
+    g.A = C; g.a_rs = ld; g.a_cs = 1;
+    g.B = V; g.b_rs = 1; g.b_cs = mrows;
+    gemm_set_C(g, Y1.p, jb);
+    const long long need = gemm_workspace_hint(g);
+    if (Wsk.n < need) Wsk.alloc(need, c.stream);
+    gemm(g, c.stream, Wsk.p, Wsk.n);
+  }
+  {  // Y2T [n2][jb] = Y1T T   (Y2 = T^T Y1)
+    GemmArgs g;
+    g.M = n2; g.N = jb; g.K = jb;
+    gemm_set_A(g, Y1.p, jb, false);
+    g.B = T; g.b_rs = ldt; g.b_cs = 1;
+    gemm_set_C(g, Y2.p, jb);
+    gemm(g, c.stream);
+  }
+  {  // C^T [n2][mrows] -= Y2T VT^T
+    GemmArgs g;
+    g.M = n2; g.N = mrows; g.K = jb;
+    gemm_set_A(g, Y2.p, jb, false);
+    g.B = VT.p; g.b_rs = 1; g.b_cs = jb;
+    g.C = C; g.c_rs = ld; g.c_cs = 1;
+    g.alpha = -1.0; g.beta = 1.0;
+    const long long need = gemm_workspace_hint(g);
+    if (Wsk.n < need) Wsk.alloc(need, c.stream);
+    gemm(g, c.stream, Wsk.p, Wsk.n);
+  }
+}
+
 void gram_vtv(Ctx& c, const double* V, int mrows, int jb, double* G, DBuf& Wsk) {  // G = V^T V (jb x jb)
   GemmArgs g;
   g.M = jb; g.N = jb; g.K = mrows;
@@ -952,7 +996,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
   }
   DBuf red(149LL * (NB + 2), c.stream), Vb((long long)m * NB, c.stream), Gram(NB * NB, c.stream),
       T(NB * NB, c.stream), Y1, Y2, Wsk;
-  DBuf Vbig, Gbig, Tbig, P1;
+  DBuf Vbig, Gbig, Tbig, P1, VTbig;
   const long long ld = m;
   for (int J0 = 0; J0 < k; J0 += NB2) {
     const int JB = std::min(NB2, k - J0);
@@ -1055,7 +1099,7 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       }
     }
     tm.mark(2);
-    apply_wy_left(c, Vbig.p, mrowsJ, JB, Tbig.p, JB, W + (long long)jend * ld + J0, ld, n2, Y1, Y2, Wsk);
+    apply_wy_left_t(c, Vbig.p, mrowsJ, JB, Tbig.p, JB, W + (long long)jend * ld + J0, ld, n2, Y1, Y2, Wsk, VTbig);
     tm.mark(5);
   }
   tm.report(m, n);
