@@ -271,3 +271,10 @@ def test_op_round_vs_reference(tt):
         ref = train(d, f"{name}_round")
         assert [c.shape for c in out.cores] == [c.shape for c in ref], name
         assert rel(O.op_full(list(out.cores)), O.op_full(ref)) <= 1e-12, name
+
+
+def test_op_to_dense_vs_oracle(tt):
+    """tt_op_to_dense via the device contraction of the fused-mode train (tt.py:566-577)."""
+    d = load("op_round.npz")
+    A = train(d, "AA_round")
+    assert rel(tt.tt_op_to_dense(tt.TTLinearOperator(A)), O.op_full(A)) <= 1e-14
