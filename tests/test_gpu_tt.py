@@ -278,3 +278,33 @@ def test_op_to_dense_vs_oracle(tt):
     d = load("op_round.npz")
     A = train(d, "AA_round")
     assert rel(tt.tt_op_to_dense(tt.TTLinearOperator(A)), O.op_full(A)) <= 1e-14
+
+
+def test_round_edge_cases_vs_oracle(tt):
+    """tt_round's special cases (tt.py:409-429): order 1 and all-ranks-1 trains return an
+    unchanged copy, the zero train becomes the canonical rank-1 zero, max_rank caps after the
+    tolerance, ranks never grow; tt_apply rejects mismatched modes."""
+    from paper_2501_12151_b200.errors import ShapeMismatchError
+    rng = np.random.default_rng(3)
+    one = [rng.standard_normal((1, 4, 1))]
+    out = tt.tt_round(tt.TensorTrain(one))
+    assert len(out.cores) == 1 and np.array_equal(out.cores[0], one[0])
+    r1 = [rng.standard_normal((1, 2, 1)) for _ in range(5)]
+    out = tt.tt_round(tt.TensorTrain(r1))
+    assert all(np.array_equal(a, b) for a, b in zip(out.cores, r1))
+    z = [np.zeros((1, 2, 3)), np.zeros((3, 2, 3)), np.zeros((3, 2, 1))]
+    out = tt.tt_round(tt.TensorTrain(z))
+    ref = O.tt_round(z)
+    assert [c.shape for c in out.cores] == [c.shape for c in ref] == [(1, 2, 1)] * 3
+    assert all(not np.any(c) for c in out.cores)
+    ranks = [1, 2, 4, 8, 8, 4, 2, 1]
+    x = [rng.standard_normal((ranks[k], 2, ranks[k + 1])) for k in range(7)]
+    for tol, cap in ((1e-12, 3), (0.3, None), (0.0, 2)):
+        out = tt.tt_round(tt.TensorTrain(x), tt.TruncationPolicy(tol, cap))
+        ref = O.tt_round(x, tol, cap)
+        assert [c.shape for c in out.cores] == [c.shape for c in ref], (tol, cap)
+        assert all(a <= b for a, b in zip([c.shape[2] for c in out.cores], ranks[1:]))
+        assert rel(O.tt_full(list(out.cores)), O.tt_full(ref)) <= 1e-11
+    A = [rng.standard_normal((1, 2, 3, 1))] + [rng.standard_normal((1, 2, 2, 1)) for _ in range(6)]
+    with pytest.raises(ShapeMismatchError):
+        tt.tt_apply(tt.TTLinearOperator(A), tt.TensorTrain(x))
