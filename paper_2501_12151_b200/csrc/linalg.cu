@@ -19,21 +19,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-wide sum with ONE barrier: every thread adds the NT/32 warp partials itself (same
-// order everywhere).  The caller must separate consecutive calls by a __syncthreads (red is
-// rewritten); the Householder loop below has two per column.
-template <int NT>
-__device__ __forceinline__ double block_sum1(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) t += red[w];
-  return t;
-}
-
 // Block-wide sum, result broadcast to every thread.  red must hold >= 33 doubles.
 template <int NT>
 __device__ double block_sum(double v, double* red) {
@@ -76,7 +61,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(CMatView in, MatView Qo, MatView
     double* vj = W + (long long)j * m;
     double part = 0.0;
     for (int i = j + 1 + tid; i < m; i += NT) part += vj[i] * vj[i];
-    const double xnorm2 = block_sum1<NT>(part, red);
+    const double xnorm2 = block_sum<NT>(part, red);
     const double alpha = vj[j];
     double t = 0.0, beta = alpha, scal = 1.0;
     if (xnorm2 > 0.0) {  // dlarfg
