@@ -123,3 +123,15 @@ def test_gpu_round_large_bond_truncating_vs_oracle():
     ref = O.tt_round(xx, 1e-10)
     assert [c.shape for c in y.cores] == [c.shape for c in ref]
     assert O.tt_norm(O.tt_sub(list(y.cores), ref)) <= 1e-12 * O.tt_norm(ref)
+
+
+@pytest.mark.gpu
+def test_gpu_sweep_tma_gemm_sizes():
+    """Ranks large enough for the TMA GEMM path (local-matvec step 1 with a transposed v, step 3
+    and the left-environment update): every y_k of the sweep vs the oracle at <= 1e-12."""
+    from paper_2501_12151_b200 import kernels, tt
+    from paper_2501_12151_b200.configs import c4_problem
+    op, x = c4_problem(128, d=9)
+    ys, _ = kernels.matvec_sweep(tt.TTLinearOperator(op), tt.TensorTrain(x))
+    for k, (y, r) in enumerate(zip(ys, O.matvec_sweep(op, x))):
+        assert y.shape == r.shape and rel(y, r) <= TOL, k
