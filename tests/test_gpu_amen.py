@@ -108,3 +108,25 @@ def test_solve_is_bitwise_reproducible():
     (x1, r1), (x2, r2) = runs
     assert r1.residual_history == r2.residual_history
     assert all(np.array_equal(a, b) for a, b in zip(x1.cores, x2.cores))
+
+
+def test_config_c2_vs_reference_ensemble():
+    """BASELINE config C2 (2^8 nodes/axis, 5.0e7 DOF, tol 1e-6, max rank 64) -- local systems up
+    to 68 x 2 x 68, so the persistent TMA CG kernel carries the solve -- against the real
+    reference's trajectory band (8 runs, tests/golden/make_c1_band.py ... C2), widened by 10%."""
+    import json
+    import os
+
+    from paper_2501_12151_b200.amen import AmenConfig, amen_solve
+    from paper_2501_12151_b200.configs import WORKLOADS, build
+    from paper_2501_12151_b200.tt import TensorTrain, TruncationPolicy, TTLinearOperator
+    from tests.golden_io import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "c2_band.json")))
+    prob, x0, kw = build(WORKLOADS["C2"])
+    rel, cap = kw.pop("rounding")
+    x, rep = amen_solve(TTLinearOperator(prob.op), TensorTrain(prob.rhs), TensorTrain(x0),
+                        AmenConfig(rounding=TruncationPolicy(rel, cap), **kw))
+    lo, hi = ref["band_final"]
+    assert 0.9 * lo <= rep.final_relative_residual <= 1.1 * hi, (rep.final_relative_residual, ref["band_final"])
+    assert rep.converged == ref["converged"]
+    assert max(x.ranks) == max(ref["ranks"])
