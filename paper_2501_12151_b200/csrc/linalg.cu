@@ -186,7 +186,7 @@ template <int NT, int GS, int KMAX, bool SMEM>
 __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, double* so, MatView Vto,
                                                     double* gws, double tol, int dbg) {
   extern __shared__ double sm[];
-  __shared__ int s_rot;
+  __shared__ int s_rot[2];  // per sweep parity: the reset of sweep s+1 cannot race the reads of sweep s
   int sweeps_done = 0;
   const int m = in.rows, n = in.cols;
   double* W = SMEM ? sm : gws;                          // m x n, column-major
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, dou
 
   const int P = n + (n & 1);  // players incl. a dummy when n is odd
   for (int sweep = 0; sweep < 80; ++sweep) {
-    if (tid == 0) s_rot = 0;
+    if (tid == 0) s_rot[sweep & 1] = 0;
     __syncthreads();
     int rotated = 0;
     for (int r = 0; r < P - 1; ++r) {
@@ -227,10 +227,10 @@ __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, dou
       }
       __syncthreads();
     }
-    if (rotated) s_rot = 1;
+    if (rotated) s_rot[sweep & 1] = 1;
     __syncthreads();
     sweeps_done = sweep + 1;
-    if (!s_rot) break;
+    if (!s_rot[sweep & 1]) break;
   }
   if (dbg && tid == 0) printf("[qtt] jacobi %dx%d sweeps %d\n", m, n, sweeps_done);
   // column norms
@@ -261,6 +261,139 @@ __global__ void __launch_bounds__(NT) jacobi_kernel(CMatView in, MatView Uo, dou
       const double* vc = V + (long long)c * n;
       for (int i = 0; i < n; ++i) Vto.p[rank * Vto.rs + i * Vto.cs] = vc[i];
     }
+  }
+}
+
+// One-sided Jacobi for the square case (the R^T of svd_tall): W (n x n) and V (n x n)
+// stacked into one column-major array, each padded to SEG = 16 K rows with zeros (zero
+// rows stay zero under rotations), column stride 2 SEG.  GS = 8 lanes own a column pair
+// and move 16-byte (double2) chunks: one group covers 16 rows per chunk, so every
+// quarter-warp access is one contiguous 128-byte line (no bank conflicts) and the
+// shared-memory instruction count is half that of scalar access.  W and V chunks are
+// loaded together (V's loads no longer wait for the rotation angle), warps whose pairs
+// are all past P/2 skip the round, and the three dot products run in two chains each.
+// (tools/svd_bench.py; ncu of the scalar kernel: issue-bound, fp64 pipe 27% active.)
+__device__ __forceinline__ bool jac_angle(double al, double be, double ga, double tol2, double& cs, double& sn) {
+  if (ga == 0.0 || !(ga * ga > tol2 * al * be)) return false;
+  const double zeta = (be - al) / (2.0 * ga);
+  const double az = fabs(zeta);
+  // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)); for huge |zeta|, t = 1 / (2 zeta)
+  const double t = az < 1e100 ? copysign(1.0 / (az + sqrt(fma(az, az, 1.0))), zeta) : 0.5 / zeta;
+  cs = 1.0 / sqrt(fma(t, t, 1.0));
+  sn = cs * t;
+  return true;
+}
+
+template <int NT, int K, bool VLATE = (K >= 7)>
+__global__ void __launch_bounds__(NT) jacobi_sq_kernel(CMatView in, MatView Uo, double* so, MatView Vto, double tol,
+                                                       int dbg) {
+  constexpr int GS = 8, SEG = 16 * K, LD = 2 * SEG;
+  extern __shared__ double sm[];
+  __shared__ int s_rot[2];  // per sweep parity: the reset of sweep s+1 cannot race the reads of sweep s
+  const int n = in.cols;
+  double* S = sm;  // n columns of LD doubles
+  double* sig = S + (long long)LD * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int gl = tid % GS, grp = tid / GS;
+  const double tol2 = tol * tol;
+  for (int e = tid; e < LD * n; e += NT) {
+    const int i = e % LD, j = e / LD;
+    double v = 0.0;
+    if (i < n) v = in.p[i * in.rs + j * in.cs];
+    else if (i >= SEG && i - SEG == j) v = 1.0;
+    S[e] = v;
+  }
+  __syncthreads();
+  int sweeps_done = 0;
+  const int P = n + (n & 1), half = P / 2;
+  const bool warp_live = warp * (32 / GS) < half;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    if (tid == 0) s_rot[sweep & 1] = 0;
+    __syncthreads();
+    int rotated = 0;
+    for (int r = 0; r < P - 1; ++r) {
+      if (warp_live) {
+        const int q = grp;
+        int a, b;
+        if (q == 0) { a = r; b = P - 1; }
+        else { a = (r + q) % (P - 1); b = (r - q + (P - 1)) % (P - 1); }
+        const bool live = q < half && a < n && b < n;
+        if (a > b) { const int t = a; a = b; b = t; }
+        if (!live) { a = 0; b = 0; }
+        double2* wa = reinterpret_cast<double2*>(S + (long long)a * LD) + gl;
+        double2* wb = reinterpret_cast<double2*>(S + (long long)b * LD) + gl;
+        // chunks 0..K-1: W rows, K..2K-1: V rows (V loaded after the angle when K = 7: the
+        // 448-thread block is capped at 128 registers)
+        constexpr int KR = VLATE ? K : 2 * K;
+        double2 x[KR], y[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          x[k] = wa[k * GS];
+          y[k] = wb[k * GS];
+        }
+        double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          al0 = fma(x[k].x, x[k].x, al0); be0 = fma(y[k].x, y[k].x, be0); ga0 = fma(x[k].x, y[k].x, ga0);
+          al1 = fma(x[k].y, x[k].y, al1); be1 = fma(y[k].y, y[k].y, be1); ga1 = fma(x[k].y, y[k].y, ga1);
+        }
+        double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        double cs, sn;
+        if (live && jac_angle(al, be, ga, tol2, cs, sn)) {
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            wa[k * GS] = make_double2(cs * x[k].x - sn * y[k].x, cs * x[k].y - sn * y[k].y);
+            wb[k * GS] = make_double2(sn * x[k].x + cs * y[k].x, sn * x[k].y + cs * y[k].y);
+          }
+          if constexpr (VLATE) {
+#pragma unroll
+            for (int k = K; k < 2 * K; ++k) {
+              const double2 u = wa[k * GS], v = wb[k * GS];
+              wa[k * GS] = make_double2(cs * u.x - sn * v.x, cs * u.y - sn * v.y);
+              wb[k * GS] = make_double2(sn * u.x + cs * v.x, sn * u.y + cs * v.y);
+            }
+          }
+          rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (rotated) s_rot[sweep & 1] = 1;
+    __syncthreads();
+    sweeps_done = sweep + 1;
+    if (!s_rot[sweep & 1]) break;
+  }
+  if (dbg && tid == 0) printf("[qtt] jacobi(sq) %dx%d sweeps %d\n", n, n, sweeps_done);
+  for (int c = warp; c < n; c += NW) {
+    const double* wc = S + (long long)c * LD;
+    double s2 = 0;
+    for (int i = lane; i < n; i += 32) s2 += wc[i] * wc[i];
+    s2 = warp_sum(s2);
+    if (lane == 0) sig[c] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int c = tid; c < n; c += NT) {
+    const double sc = sig[c];
+    int rank = 0;
+    for (int d = 0; d < n; ++d) {
+      const double sd = sig[d];
+      rank += (sd > sc) || (sd == sc && d < c);
+    }
+    so[rank] = sc;
+    const double inv = sc > 0 ? 1.0 / sc : 0.0;
+    const double* wc = S + (long long)c * LD;
+    if (Uo.p)
+      for (int i = 0; i < n; ++i)
+        Uo.p[i * Uo.rs + rank * Uo.cs] = sc > 0 ? wc[i] * inv : (i == rank ? 1.0 : 0.0);
+    if (Vto.p)
+      for (int i = 0; i < n; ++i) Vto.p[rank * Vto.rs + i * Vto.cs] = wc[SEG + i];
   }
 }
 
@@ -594,6 +727,20 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
   }
 }
 
+// n <= 16 K: 8 lanes per pair, ceil(n/2) <= 8 K pairs -> NT = 64 K threads
+template <int NT, int K>
+static void jacobi_sq_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt, double tol, size_t bytes) {
+  static_assert(NT == 64 * K, "one 8-lane group per pair");
+  static bool attr = false;
+  if (!attr) {
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_sq_kernel<NT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemDoubles * 8));
+    attr = true;
+  }
+  jacobi_sq_kernel<NT, K><<<1, NT, bytes, c.stream>>>(in, U, s, Vt, tol, jacobi_dbg());
+  QTT_CHECK_LAUNCH();
+}
+
 static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   const int m = in.rows, n = in.cols;
   static const int big_at = std::getenv("QTT_BJ_MIN") ? std::atoi(std::getenv("QTT_BJ_MIN")) : 160;
@@ -602,6 +749,21 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
     return;
   }
   const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
+  static const int sq = std::getenv("QTT_JAC_SQ") ? std::atoi(std::getenv("QTT_JAC_SQ")) : 1;
+  if (sq && m == n && n <= 112) {
+    const int K = cdiv(n, 16);
+    const size_t bytes = ((size_t)32 * K * n + n) * sizeof(double);
+    switch (K) {
+      case 1: jacobi_sq_launch<64, 1>(c, in, U, s, Vt, tol, bytes); break;
+      case 2: jacobi_sq_launch<128, 2>(c, in, U, s, Vt, tol, bytes); break;
+      case 3: jacobi_sq_launch<192, 3>(c, in, U, s, Vt, tol, bytes); break;
+      case 4: jacobi_sq_launch<256, 4>(c, in, U, s, Vt, tol, bytes); break;
+      case 5: jacobi_sq_launch<320, 5>(c, in, U, s, Vt, tol, bytes); break;
+      case 6: jacobi_sq_launch<384, 6>(c, in, U, s, Vt, tol, bytes); break;
+      default: jacobi_sq_launch<448, 7>(c, in, U, s, Vt, tol, bytes); break;
+    }
+    return;
+  }
   const int len = std::max(m, n);  // rows of W (m) and of V (n) per lane slice
   if (len <= 4 * 32)
     jacobi_launch<4, 32>(c, in, U, s, Vt, tol);

@@ -71,6 +71,20 @@ def test_svd_large_matches_numpy(tt, shape, grade):
         assert np.linalg.norm(u[:, :big].T @ u[:, :big] - np.eye(big)) <= 1e-12 * k
 
 
+@pytest.mark.parametrize("shape", [(50, 20), (120, 100)])
+def test_svd_rank_deficient(tt, shape):
+    """Exactly rank-5 input: zero singular values come out as (near) zero, U still
+    orthonormal (Jacobi columns of norm zero map to unit basis vectors)."""
+    rng = np.random.default_rng(shape[1])
+    a = rng.standard_normal((shape[0], 5)) @ rng.standard_normal((5, shape[1]))
+    u, s, vt = tt._svd(a)
+    sn = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(s - sn)) <= 1e-13 * sn[0]
+    assert rel(u @ np.diag(s) @ vt, a) <= 1e-13
+    k = min(shape)
+    assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-12 * k
+
+
 def test_qr_rank_deficient(tt):
     rng = np.random.default_rng(3)
     a = rng.standard_normal((40, 5)) @ rng.standard_normal((5, 12))
@@ -82,8 +96,12 @@ def test_qr_rank_deficient(tt):
     assert np.array_equal(r, rn) and rel(q, qn) == 0.0
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (8, 3), (3, 8), (72, 36), (200, 100), (150, 150), (30, 120)])
+@pytest.mark.parametrize("shape", [(1, 1), (8, 3), (3, 8), (72, 36), (200, 100), (150, 150), (30, 120),
+                                   (16, 16), (40, 17), (100, 45), (64, 64), (180, 75), (96, 96), (224, 112),
+                                   (300, 101), (113, 113)])
 def test_svd_matches_numpy(tt, shape):
+    """Covers every width bucket of the square-Jacobi kernel (n = 16 K, K = 1..7) and both
+    neighbours of its range."""
     rng = np.random.default_rng(shape[0] + 1000 * shape[1])
     a = rng.standard_normal(shape) * np.logspace(0, -10, shape[1])[None, :]
     u, s, vt = tt._svd(a)
