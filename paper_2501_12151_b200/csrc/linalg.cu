@@ -764,6 +764,13 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
     }
     return;
   }
+  // past one CTA's shared memory the scalar kernel would run out of global memory: the block
+  // Jacobi is 2-4.5x faster there (n = 128..159: 13.8 / 21.7 / 44.0 -> 7.2 / 8.3 / 9.7 ms,
+  // tools/svd_mid.py); below, the single CTA wins (n = 116: 3.9 vs 7.1 ms)
+  if ((long long)m * n + (long long)n * n + n > kSmemDoubles) {
+    svd_block_jacobi(c, in, U, s, Vt);
+    return;
+  }
   const int len = std::max(m, n);  // rows of W (m) and of V (n) per lane slice
   if (len <= 4 * 32)
     jacobi_launch<4, 32>(c, in, U, s, Vt, tol);
