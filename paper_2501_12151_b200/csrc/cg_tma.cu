@@ -226,12 +226,23 @@ __device__ __forceinline__ void reduce_slice(const CGTmaArgs& a, long long e0, l
     double acc[W];
 #pragma unroll
     for (int ch = 0; ch < W; ++ch) acc[ch] = 0.0;
-    for (int k = warp; k < S; k += W) {
+    // two partials per pass with all their loads issued before the adds (same add order)
+    for (int k = warp; k < S; k += 2 * W) {
       const double* pk = part + k * dim + c0;
+      const bool two = k + W < S;
+      double v0[W], v1[W];
 #pragma unroll
       for (int ch = 0; ch < W; ++ch) {
         const int el = ch * 32 + lane;
-        if (el < cnt) acc[ch] += __ldcg(pk + el);
+        v0[ch] = el < cnt ? __ldcg(pk + el) : 0.0;
+        v1[ch] = (two && el < cnt) ? __ldcg(pk + W * dim + el) : 0.0;
+      }
+#pragma unroll
+      for (int ch = 0; ch < W; ++ch) {
+        if (ch * 32 + lane < cnt) {
+          acc[ch] += v0[ch];
+          if (two) acc[ch] += v1[ch];
+        }
       }
     }
 #pragma unroll
