@@ -177,11 +177,25 @@ def cert_shapes(A_cores, x_cores, f_cores):
     return shapes
 
 
+def source_digest():
+    """sha256 over the engine sources (csrc/*.cu, *.cuh): identifies the build whose recorded
+    trajectory the CPU arm extrapolates over (a kernel change can move the trajectory)."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2501_12151_b200", "csrc", "*.cu*"))):
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()
+
+
 def cpu_baseline(trace, n_cert, shapes, sweeps, budget):
     from oracle import cpu_baseline as CB
     tables, info = CB.sample_rates(budget_s=budget)
-    secs = CB.extrapolate(trace, tables, n_cert=n_cert, cert_shapes=shapes)
+    parts = CB.extrapolate_parts(trace, tables, n_cert=n_cert, cert_shapes=shapes)
+    secs = parts["total_s"]
     return secs, {
+        "breakdown_s": {k: round(v, 2) for k, v in parts.items()},
         "cores": CB.host_cores(), "kind": "port",
         "sample": (f"oracle primitives (local matvec, env update, dense+Cholesky, SVD/QR) timed on this host at "
                    f"ranks {info['ranks']} and dense dims {info['dense_dims']} in {info['sample_s']:.1f} s, "
@@ -201,6 +215,11 @@ def run_reference(args, world, rank):
         print(json.dumps({"impl": "reference", "unavailable": f"no recorded trajectory {path}"}))
         return
     traj = json.load(open(path))
+    if traj.get("source_sha256") != source_digest():
+        # the recorded trajectory belongs to another build of the engine: refuse to extrapolate
+        print(json.dumps({"impl": "reference", "unavailable": f"{path} was recorded by another engine build "
+                          "(source digest mismatch); re-record it with bench.py"}))
+        return
     trace = np.array(traj["trace"], dtype=np.int64)
     x_ranks = traj["x_ranks"]
     xc = [np.zeros((x_ranks[k], prob.dims[k], x_ranks[k + 1])) for k in range(len(prob.dims))]
@@ -283,8 +302,11 @@ def run_ours(args, world, rank, local):
     ctx.reset_stats()
     launches0 = nat.launch_count()
     times, info = [], None
+    trace_from = 0
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for step in range(args.steps):
+            if step == args.steps - 1:  # the trajectory (cpu_baseline, trajectory file) is ONE solve's
+                trace_from = len(ctx.trace())
             ctx.flush_l2()
             barrier(world)
             ctx.synchronize()
@@ -298,7 +320,7 @@ def run_ours(args, world, rank, local):
             times.append(e0.elapsed_time(e1) / 1e3)
     launches = nat.launch_count() - launches0
     stats = ctx.stats()
-    trace = ctx.trace()
+    trace = ctx.trace()[trace_from:]
     ctx.set_profiling(False)
     x_ranks = [1] + [int(c.shape[2]) for c in dx.cores()]
     value = max_over_ranks(world, float(np.mean(times)), local)
@@ -344,8 +366,8 @@ def run_ours(args, world, rank, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": workload_config(w, {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                                          "assembly_s": round(t_asm, 2)}),
+            "config": workload_config(w),
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU", "assembly_s": round(t_asm, 2),
             "result": {"converged": info["converged"], "sweeps": info["sweeps_used"],
                        "final_relative_residual": info["final_relative_residual"], "max_rank": max(x_ranks),
                        "cg_iterations": int(stats["cg_iters"] / steps),
@@ -355,7 +377,8 @@ def run_ours(args, world, rank, local):
             "roofline": roofline}
     if rank == 0:
         line["clocks"] = clk.summary()
-        traj = {"workload": args.workload, "trace": trace.tolist(), "x_ranks": x_ranks,
+        traj = {"workload": args.workload, "source_sha256": source_digest(), "trace": trace.tolist(),
+                "x_ranks": x_ranks, "cg_iterations": int(trace[:, 10].sum()),
                 "certifications": int(stats["certifications"] / steps), "sweeps": info["sweeps_used"]}
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         json.dump(traj, open(os.path.join(ROOT, "gpurun_out", f"trajectory_{args.workload}.json"), "w"))

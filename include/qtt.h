@@ -198,6 +198,21 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
                    const qtt_amen_params* prm, const double* draws, int64_t n_draws,
                    qtt_train** x_out, qtt_amen_report* rep, int32_t* rank_hist, double* res_hist);
 
+/* One core step of the sweep (amen.py:324-390, the per-core body of _sweep) run by the
+ * engine's own per-core code on injected state -- the state-injected parity check at the
+ * headline shape.  in[0..10] are host arrays with dims in_dims[3i..3i+2]: x_k, x_nb, z_k
+ * (vector cores), phi_k, phi_k1, phiz_k, phiz_k1 (bra, op, ket), psi_k, psi_k1, psiz_k,
+ * psiz_k1 (bra, rhs, 1); nb = k+1 when forward, k-1 otherwise (amen.py:356-390).  lam_max is
+ * the running spectral bound before the step and f_norm = ||f|| (amen.py:330-337).  *out is
+ * a bundle of 7 unchained vector "cores" (read with qtt_train_shape / qtt_train_download):
+ * the new x_k, x_nb, z_k and phi, phiz, psi, psiz at the bond the step rebuilt; lam is the
+ * step's spectral estimate, rank the truncation rank of _truncated_factor (amen.py:217-234),
+ * iters the local CG iterations (0 on the direct path). */
+int qtt_amen_step(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const qtt_amen_params* prm,
+                  int sweep, int k, int forward, double lam_max, double f_norm, int n_in,
+                  const double* const* in, const int64_t* in_dims, qtt_train** out, double* lam,
+                  int* rank, int* iters);
+
 #ifdef __cplusplus
 }
 #endif

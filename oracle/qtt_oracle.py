@@ -34,7 +34,7 @@ __all__ = [
     "op_full", "env_left", "env_right", "rhs_env_left", "rhs_env_right",
     "local_rhs", "local_matvec", "local_dense", "local_diag", "mixed_residual",
     "pcg", "solve_local", "truncated_factor", "default_x0", "probe_symmetry",
-    "init_z", "residual_norm", "amen_solve", "OracleSolverError",
+    "init_z", "residual_norm", "residual_norm_streaming", "amen_solve", "OracleSolverError",
 ]
 
 
@@ -423,6 +423,45 @@ def residual_norm(op, x, f, rounding=None):
     if rounding is not None:
         r = tt_round(r, *rounding)
     nf, nr = tt_norm(f), tt_norm(r)
+    return nr / nf if nf > 0 else nr
+
+
+def residual_norm_streaming(op, x, f):
+    """||A x - f|| / ||f|| exactly as residual_norm(op, x, f) with rounding=None (amen.py:87-99:
+    tt_norm(tt_sub(tt_apply(A, x, None), f)), tt.py:330-336, 362-371, 396-406, 434-449), but
+    with each difference core formed on the fly inside the right-to-left QR sweep, so the
+    rank R*r + r_f train is never held whole (C5: ~45 GB if materialised).  Same cores, same
+    LAPACK QR (dgeqrf; only R is used, so mode="r"), same absorption order."""
+    K = len(op)
+
+    def diff_core(k):
+        y = tt_apply([op[k]], [x[k]])[0]
+        g = f[k] * (-1.0 if k == 0 else 1.0)  # tt_scale(f, -1) scales the first core
+        if K == 1:
+            return y + g
+        if k == 0:
+            return np.concatenate([y, g], axis=2)
+        if k == K - 1:
+            return np.concatenate([y, g], axis=0)
+        blk = np.zeros((y.shape[0] + g.shape[0], y.shape[1], y.shape[2] + g.shape[2]))
+        blk[: y.shape[0], :, : y.shape[2]] = y
+        blk[y.shape[0]:, :, y.shape[2]:] = g
+        return blk
+
+    carry = None
+    for k in range(K - 1, 0, -1):
+        core = diff_core(k)
+        if carry is not None:
+            core = np.tensordot(core, carry, axes=(2, 0))
+        r0, n, r1 = core.shape
+        rr = np.linalg.qr(core.reshape(r0, n * r1).T, mode="r")
+        carry = rr.T
+        del core
+    core0 = diff_core(0)
+    if carry is not None:
+        core0 = np.tensordot(core0, carry, axes=(2, 0))
+    nr = float(np.linalg.norm(core0))
+    nf = tt_norm(f)
     return nr / nf if nf > 0 else nr
 
 

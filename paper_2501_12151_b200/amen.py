@@ -100,17 +100,26 @@ class SolveReport:
 def residual_norm(A, x, f, rounding=None, ctx=None):
     """Relative residual ||A x - f|| / ||f|| (absolute when ||f|| = 0), amen.py:87-99.
 
-    The reference optionally rounds A x - f before taking the norm.  Rounding with
-    relative tolerance eps is a sequence of orthogonal projections, so it changes the
-    norm by at most eps relative (it can only lower it); the device computes the
-    unrounded norm -- through the Kronecker Gram contraction when that is provably
-    accurate, else through the exact QR sweep -- and skips the expensive rounding of
-    the rank R*r + r_f difference train.  ``rounding`` is accepted for signature parity.
+    Same semantics as the reference: with ``rounding=None`` the norm of the unrounded
+    difference train A x - f, taken on the device by the exact QR sweep over its
+    Kronecker-structured cores (no rank R*r + r_f train is materialised); with a
+    ``rounding`` policy, A x - f is formed (device tt_apply), rounded with that policy
+    (device tt_round) and its norm taken, as amen.py:95-98 does.
+
+    (amen_solve's own certifications use the unrounded exact norm: rounding at
+    0.1*tol is a sequence of orthogonal projections, so it moves the norm by at most
+    0.1*tol relative -- DESIGN.md section 4.)
     """
     if A.col_dims != x.dims or A.row_dims != f.dims:
         raise ShapeMismatchError(
             f"operator {A.row_dims}x{A.col_dims} does not fit x dims {x.dims}, f dims {f.dims}")
     ctx = ctx or nat.default_context()
+    if rounding is not None:
+        from .tt import tt_apply, tt_norm, tt_round, tt_sub
+        r = tt_round(tt_sub(tt_apply(A, x, None, ctx=ctx), f), rounding, ctx=ctx)
+        nf = tt_norm(f, ctx=ctx)
+        nr = tt_norm(r, ctx=ctx)
+        return nr / nf if nf > 0 else nr
     dA, dx, df = DeviceTrain.upload(A.cores, ctx), DeviceTrain.upload(x.cores, ctx), DeviceTrain.upload(f.cores, ctx)
     out, used = ctypes.c_double(), ctypes.c_int()
     nat.call("qtt_residual_norm", ctx.handle, dA.handle, dx.handle, df.handle, 0, ctypes.byref(out),
@@ -219,3 +228,29 @@ def amen_solve(A, f, x0=None, config=None, ctx=None):
         residual_history=info["residual_history"],
     )
     return x, report
+
+
+def _core_step(A: TTLinearOperator, f: TensorTrain, config: AmenConfig, sweep: int, k: int, forward: bool,
+               lam_max: float, f_norm: float, state, ctx=None):
+    """One core step of ``_sweep`` (amen.py:324-390) run by the engine's own per-core code on
+    injected state (qtt_amen_step) -- the state-injected parity check.  ``state`` holds the
+    11 arrays x_k, x_nb, z_k, phi_k, phi_k1, phiz_k, phiz_k1, psi_k, psi_k1, psiz_k, psiz_k1
+    (psi as (bra, rhs) or (bra, rhs, 1)); returns (outputs, info): the new x_k, x_nb, z_k and
+    phi/phiz/psi/psiz at the rebuilt bond, and {"lam", "rank", "iters"}."""
+    ctx = ctx or nat.default_context()
+    arrs = [nat.f64(a.reshape(a.shape + (1,) * (3 - a.ndim))) for a in state]
+    if len(arrs) != 11:
+        raise ValueError("the core step takes 11 state arrays")
+    ptrs = (nat._P * 11)(*[nat.dptr(a) for a in arrs])
+    dims = np.array([d for a in arrs for d in a.shape], dtype=np.int64)
+    dA, df = DeviceTrain.upload(A.cores, ctx), DeviceTrain.upload(f.cores, ctx)
+    h = ctypes.c_void_p()
+    lam, rank, iters = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    prm = _params(config)
+    nat.call("qtt_amen_step", ctx.handle, dA.handle, df.handle, ctypes.byref(prm), int(sweep), int(k),
+             1 if forward else 0, float(lam_max), float(f_norm), 11, ptrs,
+             dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(h), ctypes.byref(lam),
+             ctypes.byref(rank), ctypes.byref(iters))
+    outs = DeviceTrain(h, ctx).cores()
+    return outs, {"lam": float(lam.value), "rank": int(rank.value), "iters": int(iters.value)}
+

@@ -28,7 +28,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["ElasticityProblem", "assemble_cube", "lame_3d", "dense_reference_stiffness"]
+__all__ = ["ElasticityProblem", "assemble_cube", "lame_3d", "stiffness_qtt"]
 
 
 def lame_3d(E, nu):
@@ -289,31 +289,26 @@ def _comp_core(a, b, coef):
     return c
 
 
-def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1.0),
-                  traction=(0.0, 0.0, -1.0), patch=(0.25, 0.75), round_tol=1e-14):
-    """Clamped unit cube (x = 0 face fixed), E, nu, serial binary QTT.
-
-    layers: None (uniform E) or (cut_z, E_lo, E_hi) -- E depends on z only.
-    load:   "body"  -> constant body force ``body`` through the consistent mass;
-            "patch" -> traction ``traction`` on the x = 1 face patch y,z in ``patch``.
-    """
-    if L < 1:
-        raise ValueError("L must be >= 1")
+def _factors(L, E=1.0, layers=None):
+    """1D factor QTTs (K, M, C, C^T): x/y axes with unit weight, the z axis carries E(z)."""
     N = 2 ** L
-    lam1, mu1 = lame_3d(1.0, nu)  # per unit E; E enters through the weights
-    unit = _Const(1.0)
     wz = _Layers(*layers) if layers is not None else _Const(E)
-    K1, M1, C1 = _element_matrices_1d(N, unit)
+    K1, M1, C1 = _element_matrices_1d(N, _Const(1.0))
     Kz, Mz, Cz = _element_matrices_1d(N, wz)
-    q = {  # 1D factor QTTs, x/y axes with unit weight, z axis carries E(z)
+    q = {
         ("K", 0): _matrix_qtt(K1, L), ("M", 0): _matrix_qtt(M1, L),
         ("C", 0): _matrix_qtt(C1, L), ("Ct", 0): _matrix_qtt(C1.T.copy(), L),
         ("K", 2): _matrix_qtt(Kz, L), ("M", 2): _matrix_qtt(Mz, L),
         ("C", 2): _matrix_qtt(Cz, L), ("Ct", 2): _matrix_qtt(Cz.T.copy(), L),
     }
+    return lambda kind, axis: q[(kind, 2 if axis == 2 else 0)]
 
-    def factor(kind, axis):
-        return q[(kind, 2 if axis == 2 else 0)]
+
+def stiffness_qtt(L, nu=0.3, E=1.0, layers=None, round_tol=1e-14, factor=None):
+    """Unclamped Q1 stiffness of the unit cube as a QTT operator (component core first,
+    serial binary digits): the exact sum of 21 Kronecker terms, rounded at round_tol."""
+    lam1, mu1 = lame_3d(1.0, nu)  # per unit E; E enters through the weights
+    factor = factor or _factors(L, E, layers)
 
     def D(p, r):
         """int d_p phi_i d_r phi_j as per-axis factors."""
@@ -346,7 +341,22 @@ def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1
         for ax in range(3):
             cores += [c.copy() for c in factor(kinds[ax], ax)]
         A_raw = cores if A_raw is None else _op_add(A_raw, cores)
-    A_raw = _op_round(A_raw, round_tol)
+    return _op_round(A_raw, round_tol)
+
+
+def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1.0),
+                  traction=(0.0, 0.0, -1.0), patch=(0.25, 0.75), round_tol=1e-14):
+    """Clamped unit cube (x = 0 face fixed), E, nu, serial binary QTT.
+
+    layers: None (uniform E) or (cut_z, E_lo, E_hi) -- E depends on z only.
+    load:   "body"  -> constant body force ``body`` through the consistent mass;
+            "patch" -> traction ``traction`` on the x = 1 face patch y,z in ``patch``.
+    """
+    if L < 1:
+        raise ValueError("L must be >= 1")
+    N = 2 ** L
+    factor = _factors(L, E, layers)
+    A_raw = stiffness_qtt(L, nu, E, layers, round_tol, factor)
 
     # clamp projector P = I3 (x) diag(1 - e0) (x) I (x) I     (x = 0 face)
     eye2 = np.eye(2).reshape(1, 2, 2, 1)
@@ -382,53 +392,3 @@ def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1
             "dof": 3 * N ** 3, "cells_per_axis": N - 1, "round_tol": round_tol}
     return ElasticityProblem(L=L, op=A, rhs=f, scale=scale, dims=(3,) + (2,) * (3 * L),
                              description=desc)
-
-
-def dense_reference_stiffness(L, nu=0.3, E=1.0, layers=None):
-    """Unclamped dense 3D stiffness by an element loop (test-scale check of the
-    Kronecker assembly, L <= 3).  Trilinear hexahedra, 2x2x2 Gauss (exact for
-    the constant-E case; E per element evaluated at the element centre)."""
-    N = 2 ** L
-    h = 1.0 / (N - 1)
-    n = 3 * N ** 3
-    Kd = np.zeros((n, n))
-    g = _G2
-    wz = _Layers(*layers) if layers is not None else _Const(E)
-
-    def dof(a, i, j, k):
-        return a * N ** 3 + i * N * N + j * N + k
-
-    for ex in range(N - 1):
-        for ey in range(N - 1):
-            for ez in range(N - 1):
-                zc = (ez + 0.5) * h
-                Ee = wz(zc)
-                lam, mu = lame_3d(Ee, nu)
-                ke = np.zeros((24, 24))
-                for gx in g:
-                    for gy in g:
-                        for gz in g:
-                            B = np.zeros((6, 24))
-                            for c, (ix, iy, iz) in enumerate(
-                                    [(a, b, cc) for a in (0, 1) for b in (0, 1) for cc in (0, 1)]):
-                                fx = gx if ix else 1 - gx
-                                fy = gy if iy else 1 - gy
-                                fz = gz if iz else 1 - gz
-                                dx = (1 if ix else -1) / h * fy * fz
-                                dy = (1 if iy else -1) / h * fx * fz
-                                dz = (1 if iz else -1) / h * fx * fy
-                                B[0, 3 * c + 0] = dx
-                                B[1, 3 * c + 1] = dy
-                                B[2, 3 * c + 2] = dz
-                                B[3, 3 * c + 0], B[3, 3 * c + 1] = dy, dx
-                                B[4, 3 * c + 1], B[4, 3 * c + 2] = dz, dy
-                                B[5, 3 * c + 0], B[5, 3 * c + 2] = dz, dx
-                            Dm = np.zeros((6, 6))
-                            Dm[:3, :3] = lam
-                            Dm[np.arange(3), np.arange(3)] += 2 * mu
-                            Dm[3:, 3:] = np.eye(3) * mu
-                            ke += (h ** 3 / 8.0) * B.T @ Dm @ B
-                nodes = [(ex + a, ey + b, ez + cc) for a in (0, 1) for b in (0, 1) for cc in (0, 1)]
-                idx = [dof(comp, *nd) for nd in nodes for comp in range(3)]
-                Kd[np.ix_(idx, idx)] += ke
-    return Kd

@@ -558,6 +558,9 @@ class Solver {
   }
 
   Train run(const Train* x0, AmenResult& res);
+  // One core step on injected state (qtt_amen_step, the state-injected parity check).
+  void step_injected(int sweep, int k, bool forward, double lam_max, double nf, const std::vector<HostArray>& in,
+                     std::vector<HostArray>& out, StepInfo& info);
 
  private:
   Ctx& c_;
@@ -571,12 +574,19 @@ class Solver {
   std::vector<Env> phi_, phiz_, psi_, psiz_;
   double lam_max_ = 0.0, nf_ = 0.0;
   int sweep_ = 0;
+  double last_lam_ = 0.0;
+  int last_rank_ = 0, last_iters_ = 0;
 
   void probe_symmetry();
   Train default_x0();
   std::vector<Core> init_z();
   void full_prepass(bool forward, bool xenvs, bool zenvs);
   double sweep(bool forward);
+  bool core_step(bool forward, int k, double& est);
+  void gather_state(int k, bool forward, bool after, std::vector<HostArray>& v);
+  void maybe_dump(int k, bool forward, bool after);
+  std::vector<HostArray> dump_in_;
+  double dump_lam_in_ = 0.0;
   void env_step_left(int k, bool xenvs, bool zenvs);
   void env_step_right(int k, bool xenvs, bool zenvs);
   Env phi_left(const Env& phi, const Core& bra, int k, const Core& ket);
@@ -685,6 +695,7 @@ DBuf Solver::solve_local(int k, const DBuf& rhs, const Core& prev, double& lam) 
   LocalSystem L{pl.d.p, pl.b, pl.o, pl.k, a.d.p, A_.Ap[k].p, a.r0, a.m, a.n, a.r1, pr.d.p, pr.b, pr.o, pr.k};
   int iters = 0;
   DBuf u = solve_local_system(c_, L, rhs.p, prev.d.p, prm_, sweep_, k, lam, iters, c_.profiling);
+  last_iters_ = iters;
   const long long dim = (long long)pl.b * a.m * pr.b;
   const int path = (!prm_.local_iterative && dim <= prm_.direct_dim_cap) ? 0 : 1;
   c_.trace.push_back({sweep_, k, pl.b, a.m, pr.b, phiz_[k].b, phiz_[k + 1].b, a.r0, a.r1, path, iters});
@@ -727,16 +738,143 @@ void Solver::full_prepass(bool forward, bool xenvs, bool zenvs) {
 
 double Solver::sweep(bool forward) {
   double est = 0.0;
-  const double rel = prm_.round_tol;
-  const int cap = prm_.round_max_rank;
   for (int step = 0; step < K_; ++step) {
     const int k = forward ? step : K_ - 1 - step;
+    maybe_dump(k, forward, false);
+    const bool last = core_step(forward, k, est);
+    maybe_dump(k, forward, true);
+    if (last) break;
+  }
+  return est;
+}
+
+// Host copies of the step state: in = x_k, x_nb, z_k, phi_k, phi_k1, phiz_k, phiz_k1, psi_k,
+// psi_k1, psiz_k, psiz_k1, A_k, f_k; after = x_k, x_nb, z_k and the four environments the step rebuilt
+// (bond k+1 forward, bond k backward).  nb = k+1 forward, k-1 backward.
+void Solver::gather_state(int k, bool forward, bool after, std::vector<HostArray>& v) {
+  auto core = [&](const Core& c) {
+    HostArray h;
+    h.d0 = c.r0; h.d1 = c.m * c.n; h.d2 = c.r1;
+    h.v.resize(c.numel());
+    c.d.download(h.v.data(), c.numel());
+    v.push_back(std::move(h));
+  };
+  auto env = [&](const Env& e) {
+    HostArray h;
+    h.d0 = e.b; h.d1 = e.o; h.d2 = e.k;
+    h.v.resize((size_t)e.b * e.o * e.k);
+    e.d.download(h.v.data(), (long long)h.v.size());
+    v.push_back(std::move(h));
+  };
+  const int nb = forward ? k + 1 : k - 1;
+  core(x_[k]);
+  core(x_[nb]);
+  core(z_[k]);
+  if (!after) {
+    for (auto* e : {&phi_, &phiz_}) { env((*e)[k]); env((*e)[k + 1]); }
+    for (auto* e : {&psi_, &psiz_}) { env((*e)[k]); env((*e)[k + 1]); }
+    core(A_.cores[k]);  // the operator and rhs cores of the step, as (r0, m*n, r1): the dump
+    core(f_.cores[k]);  // is then self-contained (host assemblies can differ at round-off level)
+  } else {
+    const int b = forward ? k + 1 : k;
+    env(phi_[b]); env(phiz_[b]); env(psi_[b]); env(psiz_[b]);
+  }
+  c_.sync();
+}
+
+// QTT_DUMP_STEP="sweep,core,path": write the state before and after that core step of the
+// solve (QSTEP1 file, read by tests/golden_io.py) -- the input of the state-injected check.
+void Solver::maybe_dump(int k, bool forward, bool after) {
+  static const char* spec = std::getenv("QTT_DUMP_STEP");
+  if (!spec) return;
+  int ds = -1, dk = -1;
+  char path[512] = {0};
+  if (std::sscanf(spec, "%d,%d,%511s", &ds, &dk, path) != 3 || ds != sweep_ || dk != k) return;
+  const bool lastk = forward ? (k == K_ - 1) : (k == 0);
+  if (lastk) return;
+  if (!after) {
+    dump_in_.clear();
+    gather_state(k, forward, false, dump_in_);
+    dump_lam_in_ = lam_max_;
+    return;
+  }
+  std::vector<HostArray> out;
+  gather_state(k, forward, true, out);
+  FILE* fh = std::fopen(path, "wb");
+  if (!fh) throw Error(QTT_ERR_ARG, std::string("cannot write ") + path);
+  const int hdr[7] = {sweep_, k, forward ? 1 : 0, last_rank_, last_iters_, (int)dump_in_.size(), (int)out.size()};
+  const double sc[3] = {dump_lam_in_, nf_, last_lam_};
+  std::fwrite("QSTEP1", 1, 6, fh);
+  std::fwrite(hdr, sizeof(int), 7, fh);
+  std::fwrite(sc, sizeof(double), 3, fh);
+  for (auto* vv : {&dump_in_, &out})
+    for (auto& h : *vv) {
+      const int d[3] = {h.d0, h.d1, h.d2};
+      std::fwrite(d, sizeof(int), 3, fh);
+      std::fwrite(h.v.data(), sizeof(double), h.v.size(), fh);
+    }
+  std::fclose(fh);
+  std::fprintf(stderr, "[qtt] dumped core step (sweep %d, core %d) to %s\n", sweep_, k, path);
+}
+
+void Solver::step_injected(int sweep, int k, bool forward, double lam_max, double nf, const std::vector<HostArray>& in,
+                           std::vector<HostArray>& out, StepInfo& info) {
+  if (k < 0 || k >= K_) throw Error(QTT_ERR_ARG, "step core out of range");
+  if (forward ? (k == K_ - 1) : (k == 0)) throw Error(QTT_ERR_ARG, "state-injected step needs a neighbour core");
+  if (in.size() < 11) throw Error(QTT_ERR_ARG, "state-injected step takes 11 state arrays");
+  prepare_operator(c_, A_);
+  x_.resize(K_);
+  z_.resize(K_);
+  for (auto* e : {&phi_, &phiz_, &psi_, &psiz_}) e->resize(K_ + 1);
+  auto core = [&](const HostArray& h) {
+    Core c = make_core(c_, h.d0, h.d1, 1, h.d2);
+    c.d.upload(h.v.data(), c.numel());
+    return c;
+  };
+  auto env = [&](const HostArray& h) {
+    Env e;
+    e.b = h.d0; e.o = h.d1; e.k = h.d2;
+    e.d.alloc((long long)h.v.size(), c_.stream);
+    e.d.upload(h.v.data(), (long long)h.v.size());
+    return e;
+  };
+  const int nb = forward ? k + 1 : k - 1;
+  x_[k] = core(in[0]);
+  x_[nb] = core(in[1]);
+  z_[k] = core(in[2]);
+  phi_[k] = env(in[3]); phi_[k + 1] = env(in[4]);
+  phiz_[k] = env(in[5]); phiz_[k + 1] = env(in[6]);
+  psi_[k] = env(in[7]); psi_[k + 1] = env(in[8]);
+  psiz_[k] = env(in[9]); psiz_[k + 1] = env(in[10]);
+  const Core& a = A_.cores[k];
+  if (x_[k].m != a.n || phi_[k].o != a.r0 || phi_[k + 1].o != a.r1 || phi_[k].k != x_[k].r0 ||
+      phi_[k + 1].k != x_[k].r1 || psi_[k].o != f_.cores[k].r0 || psi_[k + 1].o != f_.cores[k].r1)
+    throw Error(QTT_ERR_SHAPE, "state-injected step: state does not fit the operator/rhs cores");
+  sweep_ = sweep;
+  lam_max_ = lam_max;
+  nf_ = nf;
+  double est = 0.0;
+  info.last = core_step(forward, k, est);
+  info.lam = last_lam_;
+  info.rank = last_rank_;
+  info.iters = last_iters_;
+  info.est = est;
+  out.clear();
+  gather_state(k, forward, true, out);
+}
+
+// The per-core body of _sweep (amen.py:324-390); returns true at the last core of the pass.
+bool Solver::core_step(bool forward, int k, double& est) {
+  const double rel = prm_.round_tol;
+  const int cap = prm_.round_max_rank;
+  {
     const int rl = x_[k].r0, m = x_[k].m, rr = x_[k].r1;
     DBuf rhs = local_rhs_(psi_[k], k, psi_[k + 1]);
     double lam = 0.0;
     c_.phase((!prm_.local_iterative && (long long)rl * m * rr <= prm_.direct_dim_cap) ? PH_DIRECT : PH_CG);
     DBuf u = solve_local(k, rhs, x_[k], lam);
     c_.phase(PH_MIXED);
+    last_lam_ = lam;
     lam_max_ = std::max(lam_max_, lam);
     const bool have_dabs = K_ > 1 && lam_max_ > 0;
     const double dabs = have_dabs ? prm_.residual_tol * nf_ / (lam_max_ * std::sqrt((double)(K_ - 1))) : 0.0;
@@ -756,7 +894,8 @@ double Solver::sweep(bool forward) {
       nrm2(c_, nz.d.p, nz.numel(), c_.scal + 12);
       z_[k] = std::move(nz);
       read_scalars(c_, c_.scal + 12, 1, &est);
-      break;
+      last_rank_ = rr;
+      return true;
     }
 
     // enrichment from the mixed x/z residual, and the truncated split of u
@@ -798,6 +937,7 @@ double Solver::sweep(bool forward) {
       w.alloc((long long)r * cols, c_.stream);
       scale_rows(c_, Vt.p, cols, s.p, r, cols, w.p, cols);
     }
+    last_rank_ = r;
     // q, R = qr([Q | enrich])
     const int acols = r + ecols;
     DBuf aug((long long)rows * acols, c_.stream);
@@ -865,7 +1005,7 @@ double Solver::sweep(bool forward) {
       c_.phase(PH_RHS);
     }
   }
-  return est;
+  return false;
 }
 
 // ------------------------------------------------------------------ driver pieces
@@ -1058,6 +1198,14 @@ Train amen_solve(Ctx& c, Train& A, const Train& f, const Train* x0, const AmenPa
                  DrawStream& draws, AmenResult& res) {
   Solver s(c, A, f, prm, draws);
   return s.run(x0, res);
+}
+
+void amen_core_step(Ctx& c, Train& A, const Train& f, const AmenParams& prm, int sweep, int k, bool forward,
+                    double lam_max, double f_norm, const std::vector<HostArray>& in, std::vector<HostArray>& out,
+                    StepInfo& info) {
+  DrawStream none;
+  Solver s(c, A, f, prm, none);
+  s.step_injected(sweep, k, forward, lam_max, f_norm, in, out, info);
 }
 
 }  // namespace qtt

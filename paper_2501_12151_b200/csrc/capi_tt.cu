@@ -1,5 +1,6 @@
 // extern "C" boundary, part 2: device-resident trains, TT algebra, dense
 // factorizations and the AMEn solve (include/qtt.h).
+#include <climits>
 #include <cmath>
 #include <vector>
 #include <cstring>
@@ -155,8 +156,18 @@ int qtt_train_load_qtt1(qtt_ctx* ctx, const char* path, int* is_operator, qtt_tr
         throw qtt::Error(QTT_ERR_FORMAT, p + ": truncated header of core " + std::to_string(k));
       const uint32_t d0 = u32(off), d1 = u32(off + 4), d2 = u32(off + 8), d3 = u32(off + 12);
       off += 16;
-      const unsigned long long size = (unsigned long long)d0 * d1 * d2 * d3;
-      if (off + 8 * size > data.size())
+      // untrusted dims: each must fit an int (core shapes are int), and the product is
+      // built with overflow checks against the bytes actually left in the file
+      if (d0 > (uint32_t)INT_MAX || d1 > (uint32_t)INT_MAX || d2 > (uint32_t)INT_MAX || d3 > (uint32_t)INT_MAX)
+        throw qtt::Error(QTT_ERR_SHAPE, p + ": invalid core dims at core " + std::to_string(k));
+      const unsigned long long avail = (data.size() - off) / 8;
+      unsigned long long size = 1;
+      bool fits = true;
+      for (uint32_t dk : {d0, d1, d2, d3}) {
+        if (dk != 0 && size > avail / dk) fits = false;
+        size *= dk;  // (only used when fits)
+      }
+      if (!fits || size > avail)
         throw qtt::Error(QTT_ERR_FORMAT, p + ": truncated values of core " + std::to_string(k));
       if (d0 < 1 || d1 < 1 || d2 < 1 || d3 < 1 || (!t.is_op && d2 != 1))
         throw qtt::Error(QTT_ERR_SHAPE, p + ": invalid core dims at core " + std::to_string(k));
@@ -412,6 +423,53 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
       if (res_hist) res_hist[s] = res.residual_history[s];
     }
     *x_out = wrap(std::move(x));
+  });
+}
+
+int qtt_amen_step(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const qtt_amen_params* prm,
+                  int sweep, int k, int forward, double lam_max, double f_norm, int n_in,
+                  const double* const* in, const int64_t* in_dims, qtt_train** out, double* lam,
+                  int* rank, int* iters) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (!A || !f || !prm || !in || !in_dims || !out) throw qtt::Error(QTT_ERR_ARG, "null argument");
+    if (!T(A).is_op) throw qtt::Error(QTT_ERR_SHAPE, "A must be a TT linear operator");
+    if (n_in != 11) throw qtt::Error(QTT_ERR_ARG, "qtt_amen_step takes 11 state arrays");
+    std::vector<qtt::HostArray> st(n_in);
+    for (int i = 0; i < n_in; ++i) {
+      for (int d = 0; d < 3; ++d)
+        if (in_dims[3 * i + d] < 1 || in_dims[3 * i + d] > INT_MAX) throw qtt::Error(QTT_ERR_SHAPE, "bad state dims");
+      st[i].d0 = (int)in_dims[3 * i];
+      st[i].d1 = (int)in_dims[3 * i + 1];
+      st[i].d2 = (int)in_dims[3 * i + 2];
+      st[i].v.assign(in[i], in[i] + (size_t)st[i].d0 * st[i].d1 * st[i].d2);
+    }
+    qtt::AmenParams p;
+    p.residual_tol = prm->residual_tol;
+    p.max_sweeps = prm->max_sweeps;
+    p.enrichment_rank = prm->enrichment_rank;
+    p.local_iterative = prm->local_iterative;
+    p.direct_dim_cap = prm->direct_dim_cap;
+    p.local_iter_cap = prm->local_iter_cap;
+    p.round_tol = prm->round_tol;
+    p.round_max_rank = prm->round_max_rank;
+    p.stagnation_strikes = prm->stagnation_strikes;
+    p.fused_cg = prm->fused_cg;
+    std::vector<qtt::HostArray> res;
+    qtt::StepInfo info;
+    qtt_train* Ah = const_cast<qtt_train*>(A);
+    qtt::amen_core_step(c, Ah->t, T(f), p, sweep, k, forward != 0, lam_max, f_norm, st, res, info);
+    qtt::Train b;  // unchained bundle of the step's outputs
+    for (auto& h : res) {
+      qtt::Core core = qtt::make_core(c, h.d0, h.d1, 1, h.d2);
+      core.d.upload(h.v.data(), core.numel());
+      b.cores.push_back(std::move(core));
+    }
+    c.sync();
+    if (lam) *lam = info.lam;
+    if (rank) *rank = info.rank;
+    if (iters) *iters = info.iters;
+    *out = wrap(std::move(b));
   });
 }
 

@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(NT, 2) cg_fused_kernel(CGFusedArgs a) {
 }  // namespace
 
 int cg_fused_grid(int device) {
-  static int cached = -1;
+  static PerDevice<int> cache(-1);
+  int& cached = cache.at(device);
   if (cached > 0) return cached;
   QTT_CUDA(cudaFuncSetAttribute(cg_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX));
   int per_sm = 0, sms = 0;

@@ -322,18 +322,24 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
     double pq = 0.0, dummy = 0.0;
     const double bq = beta;
     // this thread's element of a one-chunk slice: its q, z, p loads overlap the partial sums
+    // (first iteration: beta = 0 and q/p are never read -- q is uninitialised pool memory,
+    // where 0 * NaN would poison the solve; wi + 0 * q == wi for every finite q anyway)
     const long long me = e0 + threadIdx.x;
     const bool pre = (e1 - e0) <= NT && me < e1;
+    const bool first = bq == 0.0;
     double q0 = 0.0, z0 = 0.0, p0 = 0.0;
     if (pre) {
-      q0 = a.q[me];
       z0 = a.z[me];
-      p0 = a.p[me];
+      if (!first) {
+        q0 = a.q[me];
+        p0 = a.p[me];
+      }
     }
     reduce_slice(a, e0, e1, sred, [&](long long e, double wi) {
       const bool hit = pre && e == me;
-      const double qi = wi + bq * (hit ? q0 : a.q[e]);
-      const double pi = (hit ? z0 : a.z[e]) + bq * (hit ? p0 : a.p[e]);
+      const double qi = first ? wi : wi + bq * (hit ? q0 : a.q[e]);
+      const double zi = hit ? z0 : a.z[e];
+      const double pi = first ? zi : zi + bq * (hit ? p0 : a.p[e]);
       a.q[e] = qi;
       a.p[e] = pi;
       pq += pi * qi;
@@ -400,7 +406,8 @@ size_t cg_tma_smem(int stride, int nst) {
 int cg_tma_stages(int) { return tmafb::STAGES; }
 
 int cg_tma_grid(int device) {
-  static int cached = -1;
+  static PerDevice<int> cache(-1);
+  int& cached = cache.at(device);
   if (cached > 0) return cached;
   const size_t smem = std::getenv("QTT_TMA_ATTR_KB") ? (size_t)std::atoi(std::getenv("QTT_TMA_ATTR_KB")) * 1024
                                                      : SMEM_MAX;

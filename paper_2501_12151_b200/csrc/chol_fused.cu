@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(NT, 1) chol_fused_kernel(CholArgs a) {
 }  // namespace
 
 int chol_fused_grid(int device) {
-  static int cached = -1;
+  static PerDevice<int> cache(-1);
+  int& cached = cache.at(device);
   if (cached > 0) return cached;
   QTT_CUDA(cudaFuncSetAttribute(chol_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
   int per_sm = 0, sms = 0;

@@ -42,6 +42,24 @@ struct Error : public std::runtime_error {
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Per-device one-time state (kernel function attributes and occupancy-derived grid sizes are
+// per device; every C-ABI entry makes its context's device current first, capi.cu).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+template <class T>
+struct PerDevice {
+  T v[kMaxDevices];
+  explicit PerDevice(T init) {
+    for (auto& x : v) x = init;
+  }
+  T& operator()() { return v[current_device()]; }
+  T& at(int d) { return v[d >= 0 && d < kMaxDevices ? d : 0]; }
+};
+
 // Process-wide count of kernel launches issued by this library (reported as
 // "gpu_launches" by bench.py; every launcher calls count_launch()).
 long long launch_count();

@@ -68,7 +68,8 @@ __global__ void splitk_reduce(const double* __restrict__ ws, int splits, int M, 
 
 template <class C>
 void launch(const GemmArgs& g, int splits, int kt_per, double* ws, cudaStream_t s) {
-  static bool attr_set = false;  // per-instantiation, set once per process
+  static PerDevice<bool> attr_dev(false);  // per-instantiation, set once per device
+  bool& attr_set = attr_dev();
   if (!attr_set) {
     QTT_CUDA(cudaFuncSetAttribute(dgemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)C::SMEM));

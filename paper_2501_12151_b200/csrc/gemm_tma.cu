@@ -129,7 +129,8 @@ bool gemm_tma(const GemmArgs& g, cudaStream_t s, double* ws, long long ws_double
   if (!gemm_tma_eligible(g)) return false;
   const TmaGemmPlan p = gemm_tma_plan(g);
   if (p.splits > 1 && (ws == nullptr || ws_doubles < (long long)p.splits * g.M * g.N)) return false;
-  static bool attr = false;
+  static PerDevice<bool> attr_dev(false);
+  bool& attr = attr_dev();
   if (!attr) {
     QTT_CUDA(cudaFuncSetAttribute(tma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC::SMEM));
     attr = true;

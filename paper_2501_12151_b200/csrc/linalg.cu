@@ -684,7 +684,8 @@ void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
     return;
   }
   if (need <= kSmemDoubles) {
-    static bool attr = false;
+    static PerDevice<bool> attr_dev(false);
+    bool& attr = attr_dev();
     if (!attr) {
       QTT_CUDA(cudaFuncSetAttribute(qr_kernel<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kSmemDoubles * 8));
@@ -713,7 +714,8 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
   const long long need = (long long)m * n + (long long)n * n + n;
   if (need <= kSmemDoubles) {
     auto kern = jacobi_kernel<NT, GS, KMAX, true>;
-    static bool attr = false;
+    static PerDevice<bool> attr_dev(false);
+    bool& attr = attr_dev();
     if (!attr) {
       QTT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDoubles * 8));
       attr = true;
@@ -731,7 +733,8 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
 template <int NT, int K>
 static void jacobi_sq_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt, double tol, size_t bytes) {
   static_assert(NT == 64 * K, "one 8-lane group per pair");
-  static bool attr = false;
+  static PerDevice<bool> attr_dev(false);
+  bool& attr = attr_dev();
   if (!attr) {
     QTT_CUDA(cudaFuncSetAttribute(jacobi_sq_kernel<NT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemDoubles * 8));

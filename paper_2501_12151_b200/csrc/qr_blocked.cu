@@ -737,7 +737,8 @@ constexpr int CLUSTER_SMEM_DOUBLES = 25 * 1024;  // 200 KB of panel rows per CTA
 
 // Launch the cluster panel when the panel fits 16 CTAs' shared memory; false otherwise.
 bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s) {
-  static int ok = -1;
+  static PerDevice<int> ok_dev(-1);
+  int& ok = ok_dev();
   static const int disabled = std::getenv("QTT_PANEL_CLUSTER") && std::atoi(std::getenv("QTT_PANEL_CLUSTER")) == 0;
   if (disabled) return false;
   constexpr int CL = 16;
@@ -781,7 +782,8 @@ bool launch_panel_cluster(const PanelArgs& pa, int mrows, int jb, cudaStream_t s
 // 3 per thread; false otherwise.
 template <int RPT>
 bool launch_panel_reg_t(const PanelArgs& pa, size_t dyn, cudaStream_t s) {
-  static int ok = -1;
+  static PerDevice<int> ok_dev(-1);
+  int& ok = ok_dev();
   if (ok < 0) {
     ok = cudaFuncSetAttribute(panel_reg_kernel<RPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                  cudaSuccess &&
@@ -1029,7 +1031,8 @@ void geqrf_blocked(Ctx& c, double* W, int m, int n, double* tau) {
       if (launch_panel_reg(pa, mrows, jb, c.stream) || launch_panel_cluster(pa, mrows, jb, c.stream)) {
         have_vt = need_t;
       } else if (Gs <= 148) {
-        static bool attr = false;
+        static PerDevice<bool> attr_dev(false);
+        bool& attr = attr_dev();
         if (!attr) {
           QTT_CUDA(cudaFuncSetAttribute(panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SMEM_PANEL_DOUBLES * 8));

@@ -445,7 +445,8 @@ constexpr size_t bj_dyn_bytes() { return 2ull * BJ_CHUNK * (2 * BS + 1) * sizeof
 
 template <int BS>
 int bjacobi_launch(Ctx& c, BJArgs& a) {
-  static int max_blocks = -1;
+  static PerDevice<int> max_dev(-1);
+  int& max_blocks = max_dev.at(c.device);
   if (max_blocks < 0) {
     QTT_CUDA(cudaFuncSetAttribute(bjacobi_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)bj_dyn_bytes<BS>()));
