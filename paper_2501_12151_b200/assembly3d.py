@@ -304,11 +304,34 @@ def _factors(L, E=1.0, layers=None):
     return lambda kind, axis: q[(kind, 2 if axis == 2 else 0)]
 
 
-def stiffness_qtt(L, nu=0.3, E=1.0, layers=None, round_tol=1e-14, factor=None):
+def _rounders(rounding):
+    """(operator rounding, vector rounding) at a relative tolerance: "device" runs the
+    engine's tt_round (tt.py:409-429 semantics; R->L Householder QR, L->R one-sided Jacobi SVD
+    on the B200 -- deterministic on every B200), "host" the numpy restatement above (its
+    noise-level cuts at 1e-14 depend on the host's BLAS threading)."""
+    if rounding == "host":
+        return _op_round, _vec_round
+    if rounding != "device":
+        raise ValueError(f"rounding must be 'device' or 'host', got {rounding!r}")
+    from . import tt as T
+
+    def op(A, tol):
+        if len(A) == 1:
+            return A
+        return [np.ascontiguousarray(c) for c in T.tt_op_round(T.TTLinearOperator(A), T.TruncationPolicy(tol)).cores]
+
+    def vec(x, tol):
+        return [np.ascontiguousarray(c) for c in T.tt_round(T.TensorTrain(x), T.TruncationPolicy(tol)).cores]
+
+    return op, vec
+
+
+def stiffness_qtt(L, nu=0.3, E=1.0, layers=None, round_tol=1e-14, factor=None, rounding="host"):
     """Unclamped Q1 stiffness of the unit cube as a QTT operator (component core first,
     serial binary digits): the exact sum of 21 Kronecker terms, rounded at round_tol."""
     lam1, mu1 = lame_3d(1.0, nu)  # per unit E; E enters through the weights
     factor = factor or _factors(L, E, layers)
+    op_round, _ = _rounders(rounding)
 
     def D(p, r):
         """int d_p phi_i d_r phi_j as per-axis factors."""
@@ -341,22 +364,27 @@ def stiffness_qtt(L, nu=0.3, E=1.0, layers=None, round_tol=1e-14, factor=None):
         for ax in range(3):
             cores += [c.copy() for c in factor(kinds[ax], ax)]
         A_raw = cores if A_raw is None else _op_add(A_raw, cores)
-    return _op_round(A_raw, round_tol)
+    return op_round(A_raw, round_tol)
 
 
 def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1.0),
-                  traction=(0.0, 0.0, -1.0), patch=(0.25, 0.75), round_tol=1e-14):
+                  traction=(0.0, 0.0, -1.0), patch=(0.25, 0.75), round_tol=1e-14, rounding="device"):
     """Clamped unit cube (x = 0 face fixed), E, nu, serial binary QTT.
 
-    layers: None (uniform E) or (cut_z, E_lo, E_hi) -- E depends on z only.
-    load:   "body"  -> constant body force ``body`` through the consistent mass;
-            "patch" -> traction ``traction`` on the x = 1 face patch y,z in ``patch``.
+    layers:   None (uniform E) or (cut_z, E_lo, E_hi) -- E depends on z only.
+    load:     "body"  -> constant body force ``body`` through the consistent mass;
+              "patch" -> traction ``traction`` on the x = 1 face patch y,z in ``patch``.
+    rounding: where the round_tol roundings of the operator and load trains run (the
+              reference rounds its assembled operator with tt_op_round, elasticity.py:557-565):
+              "device" (the engine's tt_round; needs the B200) or "host" (numpy, for CPU-only
+              tooling such as the reference-ensemble scripts).
     """
     if L < 1:
         raise ValueError("L must be >= 1")
     N = 2 ** L
     factor = _factors(L, E, layers)
-    A_raw = stiffness_qtt(L, nu, E, layers, round_tol, factor)
+    _op_round, _vec_round = _rounders(rounding)
+    A_raw = stiffness_qtt(L, nu, E, layers, round_tol, factor, rounding)
 
     # clamp projector P = I3 (x) diag(1 - e0) (x) I (x) I     (x = 0 face)
     eye2 = np.eye(2).reshape(1, 2, 2, 1)
@@ -389,6 +417,6 @@ def assemble_cube(L, nu=0.3, E=1.0, layers=None, load="body", body=(0.0, 0.0, -1
     f = _vec_round(_apply(P, f), round_tol)
     f = _scale_vec(f, 1.0 / scale)
     desc = {"L": L, "nu": nu, "E": E, "layers": layers, "load": load, "layout": "serial-binary",
-            "dof": 3 * N ** 3, "cells_per_axis": N - 1, "round_tol": round_tol}
+            "dof": 3 * N ** 3, "cells_per_axis": N - 1, "round_tol": round_tol, "rounding": rounding}
     return ElasticityProblem(L=L, op=A, rhs=f, scale=scale, dims=(3,) + (2,) * (3 * L),
                              description=desc)

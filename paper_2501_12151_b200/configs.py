@@ -41,6 +41,9 @@ WORKLOADS = {
     "C2": Workload("C2", 8, 1e-6, 64),
     "C3": Workload("C3", 10, 1e-6, 96),
     "C5": Workload("C5", 9, 1e-7, 192, load="patch", layers=(0.5, 1.0, 10.0)),
+    # not a BASELINE config: the L <= 6 decompressed-field check of north_star (3 * 2^18 entries
+    # fit tt_to_dense's cap), same cube problem as C1-C3
+    "L6": Workload("L6", 6, 1e-6, 32),
 }
 
 
@@ -51,9 +54,10 @@ def x0_rank2(dims, seed=0):
     return [rng.standard_normal((1 if k == 0 else 2, dims[k], 1 if k == K - 1 else 2)) for k in range(K)]
 
 
-def build(w: Workload):
-    """Assemble (A cores, f cores, x0 cores, amen kwargs) for a workload."""
-    prob = assemble_cube(w.L, load=w.load, layers=w.layers)
+def build(w: Workload, rounding: str = "device"):
+    """Assemble (A cores, f cores, x0 cores, amen kwargs) for a workload (rounding: where the
+    assembly's 1e-14 roundings run, assembly3d.assemble_cube)."""
+    prob = assemble_cube(w.L, load=w.load, layers=w.layers, rounding=rounding)
     x0 = x0_rank2(prob.dims, 0)
     kw = dict(residual_tol=w.tol, max_sweeps=w.max_sweeps, rounding=(w.tol, w.max_rank), seed=2024)
     return prob, x0, kw

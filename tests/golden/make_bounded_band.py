@@ -39,7 +39,7 @@ OUT = os.environ.get("BAND_TMP", "/tmp/band")
 
 
 def member(i, cfg_name, k):
-    prob, x0, kw = build(WORKLOADS[cfg_name])
+    prob, x0, kw = build(WORKLOADS[cfg_name], rounding="host")
     rel, cap = kw.pop("rounding")
     kw.update(max_sweeps=k, stagnation_strikes=0)
     cfg = ram.AmenConfig(rounding=rtt.TruncationPolicy(rel, cap), **kw)

@@ -30,7 +30,7 @@ from paper_2501_12151_b200.configs import WORKLOADS, build  # noqa: E402
 
 
 def member(i, cfg_name="C1"):
-    prob, x0, kw = build(WORKLOADS[cfg_name])
+    prob, x0, kw = build(WORKLOADS[cfg_name], rounding="host")
     rel, cap = kw.pop("rounding")
     cfg = ram.AmenConfig(rounding=rtt.TruncationPolicy(rel, cap), **kw)
     if i > 0:

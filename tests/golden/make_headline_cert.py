@@ -42,7 +42,7 @@ OUT = os.path.join(HERE, "headline", "cert.json")
 def main(which):
     res = json.load(open(OUT)) if os.path.exists(OUT) else {}
     for name in which:
-        prob, _, _ = build(WORKLOADS[name])
+        prob, _, _ = build(WORKLOADS[name], rounding="host")
         x = rser.load_tt(os.path.join(HERE, "headline", f"{name.lower()}_x.qtt1"))
         A, f = rtt.TTLinearOperator(prob.op), rtt.TensorTrain(prob.rhs)
         d = {"x_ranks": list(map(int, x.ranks)), "op_ranks": list(map(int, A.ranks))}

@@ -49,7 +49,7 @@ def write_qstep(path, hdr, sc, arrays_in, arrays_out):
 def main(dump, out, cfg_name):
     st = load_qstep(dump)
     assert st["forward"], "forward steps only"
-    prob, _, kw = build(WORKLOADS[cfg_name])
+    prob, _, kw = build(WORKLOADS[cfg_name], rounding="host")
     rel, cap = kw.pop("rounding")
     cfg = ram.AmenConfig(rounding=rtt.TruncationPolicy(rel, cap), **kw)
     k, K = st["core"], len(prob.op)

@@ -44,7 +44,7 @@ def test_rigid_body_null_space(layers):
                                            (3, LAYERS, "patch"), (3, None, "patch")])
 def test_clamped_system_vs_element_loop(L, layers, load):
     """assemble_cube (clamp P K P + (I - P), scaling, load) == the oracle's clamped system."""
-    prob = assemble_cube(L, layers=layers, load=load)
+    prob = assemble_cube(L, layers=layers, load=load, rounding="host")
     K = F.stiffness(L, layers=layers)
     f = F.body_load(L) if load == "body" else F.patch_load(L)
     A, rhs, s = F.clamped_system(K, f, L)
@@ -71,6 +71,6 @@ def test_body_load_total_force():
 
 def test_operator_ranks_c1():
     """MPO ranks of the solver operator at C1 (L = 5; 45)."""
-    prob = assemble_cube(5)
+    prob = assemble_cube(5, rounding="host")
     assert max(prob.op_ranks) == 45
     assert prob.dims == (3,) + (2,) * 15

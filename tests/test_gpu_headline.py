@@ -56,7 +56,7 @@ def test_headline_certification_matches_reference(name):
     assert abs(dev - ref) <= 1e-9 * ref, (dev, ref)
     # the number the device solve reported for this x is that same certification
     solve = json.load(open(os.path.join(HEAD, f"gpu_{name.lower()}_full.json")))
-    assert abs(solve["final"] - dev) <= 1e-12 * dev, (solve["final"], dev)
+    assert abs(solve["final"] - dev) <= 1e-10, (solve["final"], dev)
 
 
 @pytest.mark.parametrize("name", ["C3", "C5"])
