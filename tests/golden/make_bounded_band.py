@@ -33,13 +33,18 @@ import ttfem.tt as rtt  # noqa: E402
 
 rtt._ALLOWED_MODES = (2, 3, 4, 8, 9)  # the 3-component leading core
 
-from paper_2501_12151_b200.configs import WORKLOADS, build  # noqa: E402
+from paper_2501_12151_b200.configs import WORKLOADS, build, x0_rank2  # noqa: E402
+from tests.golden_io import headline_inputs  # noqa: E402
 
-OUT = os.environ.get("BAND_TMP", "/tmp/band")
+OUT = os.environ.get("BAND_TMP", "/tmp/band2")
 
 
 def member(i, cfg_name, k):
-    prob, x0, kw = build(WORKLOADS[cfg_name], rounding="host")
+    # the B200's own (device-assembled, deterministic) operator and load, committed as QTT1
+    op, rhs = headline_inputs(cfg_name)
+    w = WORKLOADS[cfg_name]
+    x0 = x0_rank2([c.shape[1] for c in rhs], 0)
+    kw = dict(residual_tol=w.tol, max_sweeps=w.max_sweeps, rounding=(w.tol, w.max_rank), seed=2024)
     rel, cap = kw.pop("rounding")
     kw.update(max_sweeps=k, stagnation_strikes=0)
     cfg = ram.AmenConfig(rounding=rtt.TruncationPolicy(rel, cap), **kw)
@@ -47,7 +52,7 @@ def member(i, cfg_name, k):
         prng = np.random.default_rng(1000 + i - 1)
         x0 = [c * (1 + 1e-15 * prng.standard_normal(c.shape)) for c in x0]
     t0 = time.time()
-    x, rep = ram.amen_solve(rtt.TTLinearOperator(prob.op), rtt.TensorTrain(prob.rhs), x0=rtt.TensorTrain(x0),
+    x, rep = ram.amen_solve(rtt.TTLinearOperator(op), rtt.TensorTrain(rhs), x0=rtt.TensorTrain(x0),
                             config=cfg)
     out = {"member": i, "seconds": time.time() - t0, "converged": bool(rep.converged),
            "sweeps": int(rep.sweeps_used), "final": float(rep.final_relative_residual),

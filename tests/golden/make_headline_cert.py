@@ -34,7 +34,6 @@ import ttfem.tt as rtt  # noqa: E402
 rtt._ALLOWED_MODES = (2, 3, 4, 8, 9)
 
 from oracle import qtt_oracle as O  # noqa: E402
-from paper_2501_12151_b200.configs import WORKLOADS, build  # noqa: E402
 
 OUT = os.path.join(HERE, "headline", "cert.json")
 
@@ -42,9 +41,10 @@ OUT = os.path.join(HERE, "headline", "cert.json")
 def main(which):
     res = json.load(open(OUT)) if os.path.exists(OUT) else {}
     for name in which:
-        prob, _, _ = build(WORKLOADS[name], rounding="host")
+        # the reference's own QTT1 reader (serialize.py) loads the B200's operator, load and solution
         x = rser.load_tt(os.path.join(HERE, "headline", f"{name.lower()}_x.qtt1"))
-        A, f = rtt.TTLinearOperator(prob.op), rtt.TensorTrain(prob.rhs)
+        A = rser.load_tt(os.path.join(HERE, "headline", f"{name.lower()}_op.qtt1"))
+        f = rser.load_tt(os.path.join(HERE, "headline", f"{name.lower()}_rhs.qtt1"))
         d = {"x_ranks": list(map(int, x.ranks)), "op_ranks": list(map(int, A.ranks))}
         t0 = time.time()
         d["streaming"] = O.residual_norm_streaming(list(A.cores), list(x.cores), list(f.cores))

@@ -84,3 +84,15 @@ def step_trains(K, A_k, f_k, k):
         f.append(np.zeros((f0, n, f1)))
     return A, f
 
+
+
+def headline_inputs(name):
+    """The device-assembled operator and load of a headline config (C3, C5), as committed QTT1
+    files under tests/golden/headline/ (tools/headline_dump.py inputs): the reference-side
+    scripts solve exactly the system the B200 solved (the device assembly is deterministic;
+    host assemblies differ at round-off level)."""
+    from paper_2501_12151_b200.serialize import load_tt
+    h = os.path.join(GOLDEN, "headline")
+    A = load_tt(os.path.join(h, f"{name.lower()}_op.qtt1"))
+    f = load_tt(os.path.join(h, f"{name.lower()}_rhs.qtt1"))
+    return [np.asarray(c) for c in A.cores], [np.asarray(c) for c in f.cores]

@@ -1,5 +1,6 @@
 """GPU side of the headline parity pins (tests/test_gpu_headline.py).
 
+    python tools/headline_dump.py inputs C3|C5    # device-assembled A, f -> gpurun_out/<cfg>_{op,rhs}.qtt1
     python tools/headline_dump.py full C3|C5      # full solve, x saved as gpurun_out/<cfg>_x.qtt1
     python tools/headline_dump.py bounded C3|C5 K # K sweeps, stagnation_strikes=0 (the ensemble pin)
     QTT_DUMP_STEP=sweep,core,path python tools/headline_dump.py full C3   # + core-step state dump
@@ -23,6 +24,12 @@ from paper_2501_12151_b200.tt import TensorTrain, TruncationPolicy, TTLinearOper
 def main():
     mode, name = sys.argv[1], sys.argv[2]
     prob, x0, kw = build(WORKLOADS[name])
+    if mode == "inputs":  # the device-assembled operator and load, for the reference-side scripts
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        save_tt(TTLinearOperator(prob.op), os.path.join(ROOT, "gpurun_out", f"{name.lower()}_op.qtt1"))
+        save_tt(TensorTrain(prob.rhs), os.path.join(ROOT, "gpurun_out", f"{name.lower()}_rhs.qtt1"))
+        print(json.dumps({"mode": mode, "config": name, "op_ranks": list(prob.op_ranks)}))
+        return
     rel, cap = kw.pop("rounding")
     if mode == "bounded":
         kw.update(max_sweeps=int(sys.argv[3]), stagnation_strikes=0)
