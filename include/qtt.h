@@ -198,6 +198,15 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
                    const qtt_amen_params* prm, const double* draws, int64_t n_draws,
                    qtt_train** x_out, qtt_amen_report* rep, int32_t* rank_hist, double* res_hist);
 
+/* TT-cross (cross.py): maxvol_select (cross.py:80-115) on a tall rows x cols matrix, with the
+ * interpolation factor B = A A[piv]^-1 of the chosen rows (cross.py:202-204).  With qr != 0
+ * the matrix is first replaced by the Q factor of its thin Householder QR (the
+ * np.linalg.qr(mat) of cross.py:220, 245).  piv receives cols row indices, b rows x cols
+ * doubles (may be null), *status: 0 dominance reached, 1 rank-deficient input (pivoted-QR rows),
+ * 2 singular pivot block (pivoted-QR rows), 3 swap cap reached; | 4 if A[piv] is singular. */
+int qtt_maxvol(qtt_ctx* ctx, const double* mat, int rows, int cols, int qr, double tol, int max_iters,
+               int32_t* piv, double* b, int* status);
+
 /* One core step of the sweep (amen.py:324-390, the per-core body of _sweep) run by the
  * engine's own per-core code on injected state -- the state-injected parity check at the
  * headline shape.  in[0..10] are host arrays with dims in_dims[3i..3i+2]: x_k, x_nb, z_k

@@ -87,6 +87,8 @@ SIGNATURES = {
                                                                  ctypes.POINTER(_I)],
     "qtt_amen_solve": [_VP, _VP, _VP, _VP, ctypes.c_void_p, _P, ctypes.c_int64, ctypes.POINTER(_VP),
                        ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), _P],
+    "qtt_maxvol": [_VP, _P, _I, _I, _I, ctypes.c_double, _I, ctypes.POINTER(ctypes.c_int32), _P,
+                   ctypes.POINTER(_I)],
     "qtt_amen_step": [_VP, _VP, _VP, ctypes.c_void_p, _I, _I, _I, ctypes.c_double, ctypes.c_double, _I,
                       ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_VP), _P,
                       ctypes.POINTER(_I), ctypes.POINTER(_I)],

@@ -10,6 +10,7 @@
 #include "../../include/qtt.h"
 #include "amen.cuh"
 #include "contract.cuh"
+#include "cross.cuh"
 #include "linalg.cuh"
 #include "sweep.cuh"
 #include "capi_internal.cuh"
@@ -423,6 +424,34 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
       if (res_hist) res_hist[s] = res.residual_history[s];
     }
     *x_out = wrap(std::move(x));
+  });
+}
+
+int qtt_maxvol(qtt_ctx* ctx, const double* mat, int rows, int cols, int qr, double tol, int max_iters,
+               int32_t* piv, double* b, int* status) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (!mat || !piv || rows < 1 || cols < 1) throw qtt::Error(QTT_ERR_ARG, "maxvol: bad arguments");
+    if (rows < cols) throw qtt::Error(QTT_ERR_SHAPE, "maxvol needs a tall matrix");
+    auto dm = up(mat, (long long)rows * cols, c.stream);
+    qtt::DBuf q;
+    const double* A = dm.p;
+    if (qr) {  // thin Q (rows x cols), numpy.linalg.qr conventions
+      q.alloc((long long)rows * cols, c.stream);
+      qtt::qr(c, qtt::crowmajor(dm.p, rows, cols), qtt::rowmajor(q.p, rows, cols), qtt::MatView{});
+      A = q.p;
+    }
+    qtt::DBuf B((long long)rows * cols, c.stream);
+    int* dpiv = nullptr;
+    QTT_CUDA(cudaMallocAsync((void**)&dpiv, sizeof(int) * (cols + 1), c.stream));
+    const int st = qtt::maxvol(c, A, rows, cols, tol, max_iters, B.p, dpiv, dpiv + cols);
+    std::vector<int> hp(cols);
+    QTT_CUDA(cudaMemcpyAsync(hp.data(), dpiv, sizeof(int) * cols, cudaMemcpyDeviceToHost, c.stream));
+    if (b) B.download(b, B.n);
+    c.sync();
+    cudaFreeAsync(dpiv, c.stream);
+    for (int i = 0; i < cols; ++i) piv[i] = hp[i];
+    if (status) *status = st;
   });
 }
 

@@ -1,9 +1,9 @@
 """Run the reference's own hot-path test suites against the B200 engine.
 
-tests/ref_suite/test_amen.py and test_tt_core.py are verbatim copies of
-/root/reference/pkg/tests/test_amen.py and test_tt_core.py (reference test vectors: test
-infrastructure, not product code).  They import ``ttfem.tt``, ``ttfem.amen``,
-``ttfem.errors`` (and ``ttfem.grid`` for one operator); this conftest aliases those module
+tests/ref_suite/test_amen.py, test_tt_core.py and test_cross.py are verbatim copies of the
+reference's /root/reference/pkg/tests/ files of the same names (reference test vectors: test
+infrastructure, not product code).  They import ``ttfem.tt``, ``ttfem.amen``, ``ttfem.cross``,
+``ttfem.errors`` (and a few ``ttfem.grid`` index helpers); this conftest aliases those module
 names to the engine's drop-in modules -- the INTEGRATION.md section 1 shim -- so every
 ``amen_solve``, ``tt_round``, ``tt_apply``, ``tt_norm``... call in the suites runs on the GPU
 through libqtt.so.  All tests here are marked ``gpu``.
@@ -24,6 +24,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 from paper_2501_12151_b200 import amen as _amen  # noqa: E402
+from paper_2501_12151_b200 import cross as _cross  # noqa: E402
 from paper_2501_12151_b200 import errors as _errors  # noqa: E402
 from paper_2501_12151_b200 import tt as _tt  # noqa: E402
 
@@ -58,13 +59,41 @@ def build_shift_operator(axis, offset, d):
     return _tt.TTLinearOperator([first] + mids + [last])
 
 
+def interleave(i, j, d):
+    """Fused digits 2*i_k + j_k, most significant first (reference grid.py:120-126)."""
+    if not (0 <= i < 2 ** d and 0 <= j < 2 ** d):
+        raise ValueError("axis index out of range")
+    return tuple(2 * ((i >> (d - 1 - k)) & 1) + ((j >> (d - 1 - k)) & 1) for k in range(d))
+
+
+def deinterleave(digits):
+    """Inverse of interleave (reference grid.py:129-138)."""
+    i = j = 0
+    d = len(digits)
+    for k, t in enumerate(digits):
+        if t not in (0, 1, 2, 3):
+            raise ValueError(f"fused digit {t} out of range")
+        i += (t >> 1) << (d - 1 - k)
+        j += (t & 1) << (d - 1 - k)
+    return i, j
+
+
+def morton_index(i, j, d):
+    """Linear position of node (i, j) in the fused big-endian ordering (reference grid.py:141-146)."""
+    out = 0
+    for t in interleave(i, j, d):
+        out = 4 * out + t
+    return out
+
+
 _grid = types.ModuleType("ttfem.grid")
 _grid.build_shift_operator = build_shift_operator
+_grid.interleave, _grid.deinterleave, _grid.morton_index = interleave, deinterleave, morton_index
 _pkg = types.ModuleType("ttfem")
 _pkg.__path__ = []
-_pkg.tt, _pkg.amen, _pkg.errors, _pkg.grid = _tt, _amen, _errors, _grid
+_pkg.tt, _pkg.amen, _pkg.errors, _pkg.grid, _pkg.cross = _tt, _amen, _errors, _grid, _cross
 sys.modules.update({"ttfem": _pkg, "ttfem.tt": _tt, "ttfem.amen": _amen, "ttfem.errors": _errors,
-                    "ttfem.grid": _grid})
+                    "ttfem.grid": _grid, "ttfem.cross": _cross})
 
 # (test-id substring -> reason): deliberate, documented deviations of the engine's API
 XFAIL = {
