@@ -198,7 +198,8 @@ def cpu_baseline(trace, n_cert, shapes, sweeps, budget):
         "breakdown_s": {k: round(v, 2) for k, v in parts.items()},
         "cores": CB.host_cores(), "kind": "port",
         "sample": (f"oracle primitives (local matvec, env update, dense+Cholesky, SVD/QR) timed on this host at "
-                   f"ranks {info['ranks']} and dense dims {info['dense_dims']} in {info['sample_s']:.1f} s, "
+                   f"ranks {info['ranks']} and dense dims {info['dense_dims']} in {info['sample_s']:.1f} s plus one "
+                   f"certification-size {info['cert_unfolding']} in {info['cert_sample_s']:.1f} s, "
                    f"extrapolated over the solve's recorded trajectory ({len(trace)} local solves, "
                    f"{int(sum(int(t[10]) for t in trace))} CG iterations, {sweeps} sweeps, {n_cert} certifications)"),
     }
