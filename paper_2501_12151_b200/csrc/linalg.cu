@@ -683,6 +683,11 @@ void qr(Ctx& c, CMatView in, MatView Q, MatView R) {
     qr_large(c, in, Q, R);
     return;
   }
+  static const bool cta = !(std::getenv("QTT_QR_CTA") && std::atoi(std::getenv("QTT_QR_CTA")) == 0);
+  if (cta && n <= 256 && m <= 1024 && qr_cta_smem_doubles(m, n) * 8 <= 224 * 1024) {
+    qr_cta(c, in, Q, R);
+    return;
+  }
   if (need <= kSmemDoubles) {
     static PerDevice<bool> attr_dev(false);
     bool& attr = attr_dev();

@@ -27,6 +27,10 @@ inline CMatView cview(MatView v) { return {v.p, v.rows, v.cols, v.rs, v.cs}; }
 // have p == nullptr.  Householder reflectors with dlarfg's sign rule, Q formed
 // as in dorg2r, so Q and R match numpy.linalg.qr up to rounding.
 void qr(Ctx& c, CMatView in, MatView Q, MatView R);
+// The single-CTA blocked (compact-WY, DMMA trailing updates) kernel behind qr() for matrices whose
+// working set fits one CTA's shared memory (qr_cta.cu); qr_cta_smem_doubles(m, n) is that set.
+long long qr_cta_smem_doubles(int m, int n);
+void qr_cta(Ctx& c, CMatView in, MatView Q, MatView R);
 
 // Thin SVD of in (m x n), k = min(m, n): U (m x k), s (k, device), Vt (k x n),
 // singular values sorted descending.  Householder QR to a k x k triangle, then
