@@ -198,6 +198,10 @@ int qtt_amen_solve(qtt_ctx* ctx, const qtt_train* A, const qtt_train* f, const q
                    const qtt_amen_params* prm, const double* draws, int64_t n_draws,
                    qtt_train** x_out, qtt_amen_report* rep, int32_t* rank_hist, double* res_hist);
 
+/* tt_apply (tt.py:434-449, policy=None) into a preallocated train y whose cores have the
+ * product's shapes (e.g. a previous qtt_tt_apply result): the Kronecker cores only, no allocation. */
+int qtt_tt_apply_into(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train* y);
+
 /* TT-cross (cross.py): maxvol_select (cross.py:80-115) on a tall rows x cols matrix, with the
  * interpolation factor B = A A[piv]^-1 of the chosen rows (cross.py:202-204).  With qr != 0
  * the matrix is first replaced by the Q factor of its thin Householder QR (the

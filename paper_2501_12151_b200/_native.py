@@ -76,6 +76,7 @@ SIGNATURES = {
     "qtt_tt_dot": [_VP, _VP, _VP, _P],
     "qtt_tt_round": [_VP, _VP, ctypes.c_double, _I, ctypes.POINTER(_VP)],
     "qtt_tt_apply": [_VP, _VP, _VP, ctypes.POINTER(_VP)],
+    "qtt_tt_apply_into": [_VP, _VP, _VP, _VP],
     "qtt_tt_entries": [_VP, _VP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _P],
     "qtt_tt_to_dense": [_VP, _VP, ctypes.c_int64, _P],
     "qtt_matvec_sweep": [_VP, _VP, _VP, _I, ctypes.POINTER(_VP), _P],

@@ -272,6 +272,20 @@ int qtt_tt_apply(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train
   });
 }
 
+int qtt_tt_apply_into(qtt_ctx* ctx, const qtt_train* A, const qtt_train* x, qtt_train* y) {
+  return guarded([&] {
+    qtt::Ctx& c = C(ctx);
+    if (!y) throw qtt::Error(QTT_ERR_ARG, "null output train");
+    const qtt::Train& ta = T(A);
+    const qtt::Train& tx = T(x);
+    if (!ta.is_op || tx.is_op || y->t.is_op) throw qtt::Error(QTT_ERR_SHAPE, "operator/vector kinds");
+    for (int k = 0; k < ta.order() && k < tx.order(); ++k)
+      if (ta.cores[k].n != tx.cores[k].m) throw qtt::Error(QTT_ERR_SHAPE, "operator col_dims != vector dims");
+    qtt::tt_apply_into(c, ta, tx, y->t);
+    c.sync();
+  });
+}
+
 int qtt_tt_entries(qtt_ctx* ctx, const qtt_train* t, const int32_t* idx, int64_t count, double* out) {
   return guarded([&] {
     qtt::Ctx& c = C(ctx);

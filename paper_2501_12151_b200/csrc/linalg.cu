@@ -1,6 +1,7 @@
 // Dense FP64 kernels of the sweep (see linalg.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 
@@ -945,6 +946,84 @@ void kron_core(Ctx& c, const double* A, int Ra0, int m, int n, int Ra1, const do
   (void)total;
   kron_core_kernel<<<(int)std::min<long long>(rows, 148LL * 16), 256, staged ? sh : 0, c.stream>>>(
       A, Ra0, m, n, Ra1, x, rx0, rx1, y, staged);
+  QTT_CHECK_LAUNCH();
+}
+
+namespace {
+// All Kronecker cores of a TT-matvec in one launch (tt.py:443-447): global output row g of the
+// concatenated cores -> (core k: desc row0 <= g, row (a, xx, mm) of that core).  One WARP per
+// row (no block barriers: 8 independent write streams per CTA), the A and x slices read through
+// L1, the row (Ra1 * rx1 contiguous doubles) written with 16-byte streaming stores -- a pure HBM
+// write stream across all cores, no per-core launch gaps or tails.
+__global__ void __launch_bounds__(256) kron_all_kernel(const KronDesc* __restrict__ desc, int K,
+                                                       long long rows_total) {
+  __shared__ KronDesc sd[kKronMaxCores];
+  for (int i = threadIdx.x; i < K; i += blockDim.x) sd[i] = desc[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows_total;
+       row += nw) {
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sd[mid].row0 <= row) lo = mid; else hi = mid - 1;
+    }
+    const KronDesc& d = sd[lo];
+    const long long r = row - d.row0;
+    const int m = d.m, n = d.n, Ra1 = d.Ra1, rx1 = d.rx1;
+    const int mm = (int)(r % m);
+    const long long t = r / m;
+    const int xx = (int)(t % d.rx0), a = (int)(t / d.rx0);
+    const double* sa = d.A + ((long long)a * m + mm) * n * Ra1;
+    const double* sx = d.x + (long long)xx * n * rx1;
+    const int cols = Ra1 * rx1;
+    double* yr = d.y + r * cols;
+    if ((rx1 & 1) == 0) {
+      const int h = rx1 >> 1;
+      double2* dst = reinterpret_cast<double2*>(yr);
+      for (int e = lane; e < Ra1 * h; e += 32) {
+        const int b = e / h, j = e - b * h;
+        double s0 = 0.0, s1 = 0.0;
+        for (int nn = 0; nn < n; ++nn) {
+          const double av = __ldg(sa + nn * Ra1 + b);
+          const double2 xv = __ldg(reinterpret_cast<const double2*>(sx + nn * rx1) + j);
+          s0 = fma(av, xv.x, s0);
+          s1 = fma(av, xv.y, s1);
+        }
+        __stcs(dst + e, make_double2(s0, s1));
+      }
+    } else {
+      for (int e = lane; e < cols; e += 32) {
+        const int b = e / rx1, yy = e - b * rx1;
+        double sum = 0.0;
+        for (int nn = 0; nn < n; ++nn) sum += __ldg(sa + nn * Ra1 + b) * __ldg(sx + nn * rx1 + yy);
+        __stcs(yr + e, sum);
+      }
+    }
+  }
+}
+}  // namespace
+
+void kron_all(Ctx& c, const std::vector<KronDesc>& cores) {
+  const int K = (int)cores.size();
+  if (K == 0) return;
+  if (K > kKronMaxCores) throw Error(QTT_ERR_ARG, "kron_all: too many cores");
+  std::vector<KronDesc> d(cores);
+  long long rows = 0;
+  bool aligned = true;
+  for (auto& e : d) {
+    e.row0 = rows;
+    rows += (long long)e.Ra0 * e.rx0 * e.m;
+    if ((e.rx1 & 1) == 0 && ((reinterpret_cast<uintptr_t>(e.x) | reinterpret_cast<uintptr_t>(e.y)) & 15) != 0)
+      aligned = false;
+  }
+  if (!aligned) throw Error(QTT_ERR_ARG, "kron_all: cores must be 16-byte aligned");
+  // (a pageable source: the copy is staged before cudaMemcpyAsync returns, d may go out of scope)
+  DBuf dd((long long)((K * sizeof(KronDesc) + 7) / 8), c.stream);
+  QTT_CUDA(cudaMemcpyAsync(dd.p, d.data(), K * sizeof(KronDesc), cudaMemcpyHostToDevice, c.stream));
+  kron_all_kernel<<<(int)std::min<long long>(cdiv(rows, 8), 148LL * 8), 256, 0, c.stream>>>(
+      reinterpret_cast<const KronDesc*>(dd.p), K, rows);
   QTT_CHECK_LAUNCH();
 }
 

@@ -2,6 +2,8 @@
 // sign conventions), one-sided Jacobi SVD, blocked Cholesky + triangular solves,
 // deterministic reductions and small elementwise kernels.
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 #include "engine.cuh"
 
@@ -60,6 +62,17 @@ void read_scalars(Ctx& c, const double* dev, int n, double* host);
 // y[(a,x), m, (b,y)] = sum_n A[a,m,n,b] x[x,n,y]          (tt.py:443-447 Kronecker core)
 void kron_core(Ctx& c, const double* A, int Ra0, int m, int n, int Ra1, const double* x, int rx0,
                int rx1, double* y);
+// All Kronecker cores of a TT-matvec in one launch: core k reads A_k (Ra0, m, n, Ra1), x_k
+// (rx0, n, rx1) and writes y_k ((Ra0 rx0), m, (Ra1 rx1)); row0 is filled in by kron_all.
+constexpr int kKronMaxCores = 64;
+struct KronDesc {
+  const double* A;
+  const double* x;
+  double* y;
+  long long row0;
+  int Ra0, m, n, Ra1, rx0, rx1;
+};
+void kron_all(Ctx& c, const std::vector<KronDesc>& cores);
 // out[i*ld_out + j] = scale[i] * in[i*ld_in + j]  (rows scaled), for S V^T style products
 void scale_rows(Ctx& c, const double* in, long long ld_in, const double* scale, int rows, int cols,
                 double* out, long long ld_out);

@@ -57,6 +57,8 @@ double tt_dot(Ctx& c, const Train& a, const Train& b);
 Train tt_round(Ctx& c, const Train& a, double rel_tol, int max_rank);
 // tt.py:434-449 with policy=None (Kronecker cores, no rounding)
 Train tt_apply(Ctx& c, const Train& A, const Train& x);
+// the same into preallocated output cores of the right shapes (one launch for <= 64 cores)
+void tt_apply_into(Ctx& c, const Train& A, const Train& x, Train& y);
 // tt.py:308-336
 Train tt_sub(Ctx& c, const Train& a, const Train& b);
 Train tt_scale_copy(Ctx& c, const Train& a, double s);

@@ -314,11 +314,37 @@ Train tt_apply(Ctx& c, const Train& A, const Train& x) {
   for (int k = 0; k < A.order(); ++k) {
     const Core& a = A.cores[k];
     const Core& v = x.cores[k];
-    Core o = make_core(c, a.r0 * v.r0, a.m, 1, a.r1 * v.r1);
-    kron_core(c, a.d.p, a.r0, a.m, a.n, a.r1, v.d.p, v.r0, v.r1, o.d.p);
-    y.cores.push_back(std::move(o));
+    y.cores.push_back(make_core(c, a.r0 * v.r0, a.m, 1, a.r1 * v.r1));
   }
+  tt_apply_into(c, A, x, y);
   return y;
+}
+
+void tt_apply_into(Ctx& c, const Train& A, const Train& x, Train& y) {
+  const int K = A.order();
+  if (x.order() != K || y.order() != K) throw Error(QTT_ERR_SHAPE, "tt_apply: order mismatch");
+  for (int k = 0; k < K; ++k) {
+    const Core& a = A.cores[k];
+    const Core& v = x.cores[k];
+    const Core& o = y.cores[k];
+    if (o.r0 != a.r0 * v.r0 || o.m != a.m || o.n != 1 || o.r1 != a.r1 * v.r1)
+      throw Error(QTT_ERR_SHAPE, "tt_apply: output core " + std::to_string(k) + " has the wrong shape");
+  }
+  if (K <= kKronMaxCores) {  // one launch for the whole train
+    std::vector<KronDesc> d;
+    for (int k = 0; k < K; ++k) {
+      const Core& a = A.cores[k];
+      const Core& v = x.cores[k];
+      d.push_back(KronDesc{a.d.p, v.d.p, y.cores[k].d.p, 0, a.r0, a.m, a.n, a.r1, v.r0, v.r1});
+    }
+    kron_all(c, d);
+    return;
+  }
+  for (int k = 0; k < K; ++k) {
+    const Core& a = A.cores[k];
+    const Core& v = x.cores[k];
+    kron_core(c, a.d.p, a.r0, a.m, a.n, a.r1, v.d.p, v.r0, v.r1, y.cores[k].d.p);
+  }
 }
 
 Train tt_sub(Ctx& c, const Train& a, const Train& b) {

