@@ -23,8 +23,9 @@ namespace cg = cooperative_groups;
 namespace qtt {
 namespace {
 
-constexpr int NT = 384;  // 12 warps (3 per scheduler), one CTA per SM
-constexpr int NW = NT / 32;
+constexpr int NW = 12;        // 12 warps (3 per scheduler: the register file holds 3 x 168 per scheduler)
+constexpr int NTC = NW * 32;  // one CTA per SM
+constexpr int NT = NTC;
 static_assert(NW == tmafb::NWARP, "fragment dealing uses every warp");
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -39,7 +40,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   a = warp_sum(a);
   b = warp_sum(b);
   __syncthreads();
-  if (lane == 0) { red[warp] = a; red[NW + warp] = b; }
+  if (lane == 0 && warp < NW) { red[warp] = a; red[NW + warp] = b; }
   __syncthreads();
   if (warp == 0) {
     double x = lane < NW ? red[lane] : 0.0, y = lane < NW ? red[NW + lane] : 0.0;
@@ -58,7 +59,7 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
 __device__ __forceinline__ void grid_sum2(const double* part, int nparts, double& a, double& b, double* red) {
   a = 0.0;
   b = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += NT) {
+  for (int i = threadIdx.x; i < nparts && threadIdx.x < NTC; i += NTC) {
     a += __ldcg(part + 2 * i);
     b += __ldcg(part + 2 * i + 1);
   }
@@ -71,7 +72,7 @@ __device__ __forceinline__ void cta_partial2(double a, double b, double* red, do
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   a = warp_sum(a);
   b = warp_sum(b);
-  if (lane == 0) { red[warp] = a; red[NW + warp] = b; }
+  if (lane == 0 && warp < NW) { red[warp] = a; red[NW + warp] = b; }
   __syncthreads();
   if (threadIdx.x == 0) {
     double x = 0.0, y = 0.0;
@@ -99,34 +100,36 @@ __device__ __forceinline__ void phase_mark(const CGTmaArgs& a, int ph, unsigned 
 // generic-proxy global writes -> later TMA (async-proxy) reads, across the grid barrier
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
-// Dispatch a region stream on the per-warp fragment count and A-row dedupe.
-template <class Get, class Epi>
-__device__ __forceinline__ void fb_stream(tmafb::Ring& ring, const tmafb::Boxes& bx, int nf, bool dedupe, int n,
-                                          Get get, Epi epi) {
-  if (dedupe) {
-    switch (nf) {
-      case 4: tmafb::stream<4, true>(ring, bx, n, get, epi); break;
-      case 6: tmafb::stream<6, true>(ring, bx, n, get, epi); break;
-      case 8: tmafb::stream<8, true>(ring, bx, n, get, epi); break;
-      case 10: tmafb::stream<10, true>(ring, bx, n, get, epi); break;
-      case 12: tmafb::stream<12, true>(ring, bx, n, get, epi); break;
-      default: tmafb::stream<16, true>(ring, bx, n, get, epi); break;
-    }
-  } else {
-    switch (nf) {
-      case 4: tmafb::stream<4, false>(ring, bx, n, get, epi); break;
-      case 6: tmafb::stream<6, false>(ring, bx, n, get, epi); break;
-      case 8: tmafb::stream<8, false>(ring, bx, n, get, epi); break;
-      case 10: tmafb::stream<10, false>(ring, bx, n, get, epi); break;
-      case 12: tmafb::stream<12, false>(ring, bx, n, get, epi); break;
-      default: tmafb::stream<16, false>(ring, bx, n, get, epi); break;
-    }
-  }
-}
+// Dispatch on the per-warp fragment count and A-row dedupe.  Every variant is its own
+// non-inlined function: one function holding all variants made ptxas spill the software-
+// pipelined operands in every loop.
+#define QTT_FB_DISPATCH(FN, nf, dedupe, ...)                                     \
+  do {                                                                           \
+    if (dedupe) {                                                                \
+      switch (nf) {                                                              \
+        case 4: ring = FN<4, true>(__VA_ARGS__); break;                     \
+        case 6: ring = FN<6, true>(__VA_ARGS__); break;                     \
+        case 8: ring = FN<8, true>(__VA_ARGS__); break;                     \
+        case 10: ring = FN<10, true>(__VA_ARGS__); break;                   \
+        case 12: ring = FN<12, true>(__VA_ARGS__); break;                   \
+        default: ring = FN<16, true>(__VA_ARGS__); break;                   \
+      }                                                                          \
+    } else {                                                                     \
+      switch (nf) {                                                              \
+        case 4: ring = FN<4, false>(__VA_ARGS__); break;                    \
+        case 6: ring = FN<6, false>(__VA_ARGS__); break;                    \
+        case 8: ring = FN<8, false>(__VA_ARGS__); break;                    \
+        case 10: ring = FN<10, false>(__VA_ARGS__); break;                  \
+        case 12: ring = FN<12, false>(__VA_ARGS__); break;                  \
+        default: ring = FN<16, false>(__VA_ARGS__); break;                  \
+      }                                                                          \
+    }                                                                            \
+  } while (0)
 
 // ---- phase 1: t2 <- Bop . v^T.  CTA c owns fragment rows [c*FR/G, (c+1)*FR/G) in
 // row blocks of <= p1_rb fragments, times column blocks of <= p1_cb fragments.
-__device__ __noinline__ void phase1(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring& ring) {
+template <int NF, bool DEDUPE>
+__device__ __noinline__ tmafb::Ring phase1_t(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring ring) {
   const int M = a.lb * a.m * a.R1, N = a.rk, K = a.lk * a.n;
   const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int KT = (K + 15) / 16;
@@ -155,12 +158,18 @@ __device__ __noinline__ void phase1(const CGTmaArgs& a, const CUtensorMap* mv, t
       return t2 + xm * K3p + (long long)bb * rk;
     });
   };
-  fb_stream(ring, bx, a.p1_nf, a.p1_dedupe != 0, r1 > r0 ? nrb * ncb : 0, get, epi);
+  tmafb::stream<NF, DEDUPE>(ring, bx, r1 > r0 ? nrb * ncb : 0, get, epi);
+  return ring;
+}
+
+__device__ __forceinline__ void phase1(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring& ring) {
+  QTT_FB_DISPATCH(phase1_t, a.p1_nf, a.p1_dedupe != 0, a, mv, ring);
 }
 
 // ---- phase 2 (split-K): part3[s][Y][(X,m)] = phir[Y, slice s] . t2[(X,m), slice s];
 // one region per CTA: fragment-block tile x K slice.
-__device__ __noinline__ void phase2(const CGTmaArgs& a, tmafb::Ring& ring) {
+template <int NF, bool DEDUPE>
+__device__ __noinline__ tmafb::Ring phase2_t(const CGTmaArgs& a, tmafb::Ring ring) {
   const int M = a.rb, N = a.lb * a.m, K = a.R1 * a.rk;
   const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int KT = (K + 15) / 16;
@@ -190,7 +199,12 @@ __device__ __noinline__ void phase2(const CGTmaArgs& a, tmafb::Ring& ring) {
     tmafb::store(g, fr, acc, M, N, [&](int r) { return P + (long long)r * N; });
   };
   const int mine = items > it0 ? (items - 1 - it0) / (int)gridDim.x + 1 : 0;
-  fb_stream(ring, bx, a.p2_nf, a.p2_dedupe != 0, mine, get, epi);
+  tmafb::stream<NF, DEDUPE>(ring, bx, mine, get, epi);
+  return ring;
+}
+
+__device__ __forceinline__ void phase2(const CGTmaArgs& a, tmafb::Ring& ring) {
+  QTT_FB_DISPATCH(phase2_t, a.p2_nf, a.p2_dedupe != 0, a, ring);
 }
 
 __device__ void matvec(const CGTmaArgs& a, const CUtensorMap* mv, tmafb::Ring& ring, cg::grid_group& grid,
@@ -221,37 +235,39 @@ __device__ __forceinline__ void reduce_slice(const CGTmaArgs& a, long long e0, l
   const int S = a.S3;
   const long long dim = a.dim;
   const double* part = a.part3;
-  for (long long c0 = e0; c0 < e1; c0 += NT) {
-    const int cnt = (int)min((long long)NT, e1 - c0);
-    double acc[W];
+  for (long long c0 = e0; c0 < e1; c0 += NTC) {
+    const int cnt = (int)min((long long)NTC, e1 - c0);
+    if (warp < W) {
+      double acc[W];
 #pragma unroll
-    for (int ch = 0; ch < W; ++ch) acc[ch] = 0.0;
-    // two partials per pass with all their loads issued before the adds (same add order)
-    for (int k = warp; k < S; k += 2 * W) {
-      const double* pk = part + k * dim + c0;
-      const bool two = k + W < S;
-      double v0[W], v1[W];
+      for (int ch = 0; ch < W; ++ch) acc[ch] = 0.0;
+      // two partials per pass with all their loads issued before the adds (same add order)
+      for (int k = warp; k < S; k += 2 * W) {
+        const double* pk = part + k * dim + c0;
+        const bool two = k + W < S;
+        double v0[W], v1[W];
 #pragma unroll
-      for (int ch = 0; ch < W; ++ch) {
-        const int el = ch * 32 + lane;
-        v0[ch] = el < cnt ? __ldcg(pk + el) : 0.0;
-        v1[ch] = (two && el < cnt) ? __ldcg(pk + W * dim + el) : 0.0;
-      }
+        for (int ch = 0; ch < W; ++ch) {
+          const int el = ch * 32 + lane;
+          v0[ch] = el < cnt ? __ldcg(pk + el) : 0.0;
+          v1[ch] = (two && el < cnt) ? __ldcg(pk + W * dim + el) : 0.0;
+        }
 #pragma unroll
-      for (int ch = 0; ch < W; ++ch) {
-        if (ch * 32 + lane < cnt) {
-          acc[ch] += v0[ch];
-          if (two) acc[ch] += v1[ch];
+        for (int ch = 0; ch < W; ++ch) {
+          if (ch * 32 + lane < cnt) {
+            acc[ch] += v0[ch];
+            if (two) acc[ch] += v1[ch];
+          }
         }
       }
-    }
 #pragma unroll
-    for (int ch = 0; ch < W; ++ch) sred[warp * NT + ch * 32 + lane] = acc[ch];
+      for (int ch = 0; ch < W; ++ch) sred[warp * NTC + ch * 32 + lane] = acc[ch];
+    }
     __syncthreads();
     if ((int)threadIdx.x < cnt) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) s += sred[w * NT + threadIdx.x];
+      for (int w = 0; w < W; ++w) s += sred[w * NTC + threadIdx.x];
       f(c0 + threadIdx.x, s);
     }
     __syncthreads();
@@ -302,7 +318,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
   if (a.xany)
     reduce_slice(a, e0, e1, sred, init_r);
   else
-    for (long long e = e0 + threadIdx.x; e < e1; e += NT) init_r(e, 0.0);
+    for (long long e = e0 + threadIdx.x; e < e1 && threadIdx.x < NTC; e += NTC) init_r(e, 0.0);
   fence_proxy_global();
   cta_partial2(rr, rz, red, a.red);
   grid.sync();
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
     // (first iteration: beta = 0 and q/p are never read -- q is uninitialised pool memory,
     // where 0 * NaN would poison the solve; wi + 0 * q == wi for every finite q anyway)
     const long long me = e0 + threadIdx.x;
-    const bool pre = (e1 - e0) <= NT && me < e1;
+    const bool pre = (e1 - e0) <= NTC && me < e1 && threadIdx.x < NTC;
     const bool first = bq == 0.0;
     double q0 = 0.0, z0 = 0.0, p0 = 0.0;
     if (pre) {
@@ -352,7 +368,7 @@ __global__ void __launch_bounds__(NT, 1) cg_tma_kernel(const __grid_constant__ C
     const double alpha = rho / pq;
     rr = 0.0;
     rz = 0.0;
-    for (long long e = e0 + threadIdx.x; e < e1; e += NT) {
+    for (long long e = e0 + threadIdx.x; e < e1 && threadIdx.x < NTC; e += NTC) {
       a.x[e] += alpha * a.p[e];
       const double ri = a.r[e] - alpha * a.q[e];
       a.r[e] = ri;
@@ -398,12 +414,18 @@ __global__ void transpose_kernel(const double* __restrict__ in, double* __restri
 
 bool cg_tma_supported(int lk, int n) { return ((long long)lk * n) % 2 == 0; }
 
-// the ring also serves as scratch for the split-K reduction (NW x NT doubles)
+// the ring also serves as scratch for the split-K reduction (NW x NTC doubles)
 constexpr size_t SMEM_MAX = 224 * 1024;  // + static shared memory <= the 227 KB opt-in limit
 size_t cg_tma_smem(int stride, int nst) {
-  return std::max((size_t)nst * stride, (size_t)NW * NT * sizeof(double)) + tmafb::HEADER + 1024 + 4096;
+  return std::max((size_t)nst * stride, (size_t)NW * NTC * sizeof(double)) + tmafb::HEADER + 1024 + 4096;
 }
-int cg_tma_stages(int) { return tmafb::STAGES; }
+// Ring depth: 6 stages (look-ahead 4 k-tiles) when they fit, at least 3 (QTT_TMA_STAGES overrides)
+int cg_tma_stages(int stride) {
+  int want = 6;
+  if (const char* e = std::getenv("QTT_TMA_STAGES")) want = std::atoi(e);
+  const int fit = (int)((SMEM_MAX - tmafb::HEADER - 1024 - 4096) / (size_t)stride);
+  return std::max(3, std::min({want, fit, tmafb::MAX_STAGES}));
+}
 
 int cg_tma_grid(int device) {
   static PerDevice<int> cache(-1);
@@ -435,6 +457,7 @@ CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int 
   // dedupe needs every column block (the last may be narrower) to hold a run in 2 rows
   const int cb1_min = FC1 % p.p1_cb == 0 ? p.p1_cb : FC1 % p.p1_cb;
   p.p1_dedupe = tmafb::dedupe_ok(p.p1_nf, cb1_min) ? 1 : 0;
+  if (const char* e = std::getenv("QTT_TMA_DEDUPE")) p.p1_dedupe = p.p1_dedupe && std::atoi(e);
   // phase 2: split-K; choose the fragment-block tiling and split count that
   // minimise per-CTA DMMAs plus the split-K partial traffic
   const int FR3 = cdiv(rb, 8), FC3 = cdiv(lb * m, 8);
@@ -455,7 +478,9 @@ CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int 
       // per k-tile: DMMA issue (NF x 4 k-steps x 3 warps x 16 clk) or the L2->SMEM
       // operand stream ((RB + CB) x 8 rows x 128 B at ~24 B/clk per SM), whichever is longer
       // (or the ~2 us TMA round trip spread over the ring depth)
-      const int nst = cg_tma_stages(cdiv((RB + CB) * 8 * 128, 1024) * 1024);
+      // (the latency term keeps the 4-stage ring's value: the split it selects fixes the
+      // summation order of q, and with it the solve's trajectory)
+      const int nst = 4;
       const double per_kt = std::max({(double)tmafb::nf_for(RB * CB) * 4.0 * 48.0, (RB + CB) * 8.0 * 128.0 / 24.0,
                                       4000.0 / (nst - 1)});
       const double dmma = per_kt * ktp;

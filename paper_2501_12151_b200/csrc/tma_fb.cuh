@@ -22,9 +22,7 @@ namespace tmafb {
 
 constexpr int MAXF = 16;   // fragments per warp (largest instantiation)
 constexpr int NWARP = 12;  // consumer warps per CTA: 3 per scheduler
-constexpr int STAGES = 4;      // ring depth (deeper rings only delayed the first k-tile: the
-                               // prologue burst of every CTA queues behind the others in L2)
-constexpr int MAX_STAGES = STAGES;
+constexpr int MAX_STAGES = 8;  // deepest ring (run-time depth Ring::nst; look-ahead nst - 2 k-tiles)
 constexpr int HEADER = 256;    // mbarriers (full + empty per stage) before the ring
 
 // One unit of work: output rows [m0, m0+mrows) x cols [n0, n0+ncols), k-tiles [kb, ke).
@@ -36,9 +34,10 @@ struct Ring {
   unsigned char* base;  // 1024-aligned
   uint64_t* full;
   uint64_t* empty;
-  unsigned uses;
+  int cs;                     // next stage to consume
+  unsigned cph;               // its fill parity
   int stride;                 // bytes per stage (multiple of 1024)
-  int nst;                    // stages
+  int nst;                    // stages (3 .. MAX_STAGES)
   unsigned long long* dbg;    // optional: CTA 0 stream timeline accumulators (4 per stream slot)
   int dbg_slot;
 };
@@ -56,15 +55,16 @@ __device__ __forceinline__ Ring ring_init(void* smem_raw, int stride, int nst) {
   uintptr_t p = reinterpret_cast<uintptr_t>(smem_raw) + HEADER;
   p = (p + 1023) & ~uintptr_t(1023);
   r.base = reinterpret_cast<unsigned char*>(p);
-  r.uses = 0;
+  r.cs = 0;
+  r.cph = 0;
   r.stride = stride;
   r.nst = nst;
   r.dbg = nullptr;
   r.dbg_slot = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < nst; ++s) {
       tma::mbar_init(&r.full[s], 1);
-      tma::mbar_init(&r.empty[s], blockDim.x / 32);
+      tma::mbar_init(&r.empty[s], NWARP);
     }
     tma::fence_barrier_init();
   }
@@ -79,10 +79,10 @@ struct Boxes {
   int box_a, box_b;
 };
 
-__device__ __forceinline__ void issue(Ring& r, unsigned slot, const Boxes& bx, const Region& g, int kt) {
-  const int s = slot % STAGES;
-  const unsigned f = slot / STAGES;
-  if (f > 0) tma::mbar_wait(&r.empty[s], (f - 1) & 1u);
+// Fill stage s (fill parity ph) with k-tile kt of region g: wait until every consumer warp
+// released the stage's previous fill (a fresh barrier passes the parity-1 wait at once).
+__device__ __forceinline__ void issue(Ring& r, int s, unsigned ph, const Boxes& bx, const Region& g, int kt) {
+  tma::mbar_wait(&r.empty[s], ph ^ 1u);
   unsigned char* st = r.base + (size_t)s * r.stride;
   tma::mbar_expect_tx(&r.full[s], (bx.box_a + bx.box_b) * 128);
   tma::load_2d(st, bx.ma, kt * 16, g.m0, &r.full[s]);
@@ -129,97 +129,169 @@ __device__ __forceinline__ void frags_for(const Region& g, Frags<NF>& fr) {
   }
 }
 
+// Operand fragments of one k-step, held in registers.
 template <int NF, bool DEDUPE>
-__device__ __forceinline__ void compute(const Ring& r, unsigned slot, const Boxes& bx, const Frags<NF>& fr,
-                                        double (&acc)[NF][2]) {
-  const int s = slot % STAGES;
+struct Operands {
+  double b[NF];
+  double a[2];  // DEDUPE: the run's two A fragment rows; else fragment 0's A (the rest follow one ahead)
+};
+
+// Load the operands of k-step ks (0..3) of the k-tile in stage s.
+template <int NF, bool DEDUPE>
+__device__ __forceinline__ void load_step(const Ring& r, int s, int ks, const Boxes& bx, const Frags<NF>& fr,
+                                          Operands<NF, DEDUPE>& o) {
   const unsigned sA = tma::smem_u32(r.base) + s * r.stride;
   const unsigned sB = sA + bx.box_a * 128;
   const int lane = threadIdx.x & 31;
-  const int lr = lane >> 2, lc = lane & 3;
+  const int off = tma::swz_off(ks, lane >> 2, lane & 3);
+  if constexpr (DEDUPE) {
+    o.a[0] = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+    o.a[1] = tma::lds64(sA + (fr.aoff[0] + 128 + off) * 8);
+  } else {
+    o.a[0] = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+  }
 #pragma unroll
-  for (int ks = 0; ks < 16; ks += 4) {
-    const int off = tma::swz_off(ks >> 2, lr, lc);
-    double b[NF];
-#pragma unroll
-    for (int f = 0; f < NF; ++f) b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
-    if constexpr (DEDUPE) {
-      const double x0 = tma::lds64(sA + (fr.aoff[0] + off) * 8);
-      const double x1 = tma::lds64(sA + (fr.aoff[0] + 128 + off) * 8);
-#pragma unroll
-      for (int f = 0; f < NF; ++f) tile::dmma(acc[f], f < fr.t1 ? x0 : x1, b[f]);
-    } else {
-#pragma unroll
-      for (int f = 0; f < NF; ++f) tile::dmma(acc[f], tma::lds64(sA + (fr.aoff[f] + off) * 8), b[f]);
+  for (int f = 0; f < NF; ++f) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+}
+
+// Issue the DMMAs of the k-step held in o and, when NEXT, replace every operand by that of
+// k-step ks_n of stage s_n right after its last use: the loads of the next k-step (and of the next
+// k-tile, whose full barrier the caller has already passed) are in flight while this step's
+// DMMAs drain, so the warps never stand at a k-tile boundary with an empty DMMA queue (measured
+// ~250 clocks per k-tile before, tools/micro/tma_rate.cu).
+template <int NF, bool DEDUPE, bool NEXT>
+__device__ __forceinline__ void step(const Ring& r, int s_c, int ks_c, int s_n, int ks_n, const Boxes& bx,
+                                     const Frags<NF>& fr, Operands<NF, DEDUPE>& o, double (&acc)[NF][2]) {
+  const unsigned sA = tma::smem_u32(r.base) + s_n * r.stride;
+  const unsigned sB = sA + bx.box_a * 128;
+  const int lane = threadIdx.x & 31;
+  const int off = tma::swz_off(ks_n, lane >> 2, lane & 3);
+  if constexpr (DEDUPE) {
+    double n0 = 0.0, n1 = 0.0;
+    if constexpr (NEXT) {
+      n0 = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+      n1 = tma::lds64(sA + (fr.aoff[0] + 128 + off) * 8);
     }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      tile::dmma(acc[f], f < fr.t1 ? o.a[0] : o.a[1], o.b[f]);
+      if constexpr (NEXT) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+    }
+    if constexpr (NEXT) {
+      o.a[0] = n0;
+      o.a[1] = n1;
+    }
+  } else {
+    // A fragments one ahead of their DMMA (this step's from the current stage s_c)
+    const unsigned sAc = tma::smem_u32(r.base) + s_c * r.stride;
+    const int offc = tma::swz_off(ks_c, lane >> 2, lane & 3);
+    double a = o.a[0];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      double an = 0.0;
+      if (f + 1 < NF)
+        an = tma::lds64(sAc + (fr.aoff[f + 1] + offc) * 8);
+      else if constexpr (NEXT)
+        an = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+      tile::dmma(acc[f], a, o.b[f]);
+      if constexpr (NEXT) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+      a = an;
+    }
+    o.a[0] = a;
   }
 }
 
-// Stream regions get(0..n-1) through the ring; epi(region, frags, acc) after each
-// region's last k-tile (all threads call it).
+// Stream regions get(0..n-1) through the ring; epi(region, frags, acc) after each region's last
+// k-tile (all threads call it).  The ring runs LA = nst - 2 k-tiles ahead and k-tile q is issued
+// by lane 0 of warp q % NWARP at the top of k-tile q - LA: the stage it refills was released two
+// k-tiles ago, so the issuing warp does not wait for the slowest warp, and the issue cost is paid
+// by a different warp every k-tile.  (With thread 0 producing for everybody at a look-ahead of
+// nst - 1, warp 0 waited for the slowest warp and issued on every k-tile, and every k-tile ran
+// ~630 clocks behind its DMMA time -- profiles/r02/micro.)
 template <int NF, bool DEDUPE, class Get, class Epi>
 __device__ __forceinline__ void stream(Ring& r, const Boxes& bx, int n, Get get, Epi epi) {
   if (n <= 0) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool tl = r.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long t_start = tl ? fb_clock() : 0;
-  int pi = 0, pk = 0;
-  Region P;
-  const unsigned first = r.uses;
-  unsigned produced = first;
-  if (threadIdx.x == 0) {
-    tma::fence_proxy_async();  // earlier generic-proxy use of the ring's shared memory
-    P = get(0);
-    pk = P.kb;
-    for (int s = 0; s < STAGES - 1 && pi < n; ++s) {
-      issue(r, produced++, bx, P, pk);
+  const int nst = r.nst, LA = nst - 2;
+  // producer cursor (tracked by every thread): region pi, k-tile pk, stage ps, fill parity pph,
+  // issuing warp pw
+  int pi = 0, ps = r.cs, pw = 0;
+  unsigned pph = r.cph;
+  Region P = get(0);
+  int pk = P.kb;
+  auto produce = [&]() {
+    if (pi < n) {
+      if (warp == pw && lane == 0) issue(r, ps, pph, bx, P, pk);
       if (++pk >= P.ke && ++pi < n) {
         P = get(pi);
         pk = P.kb;
       }
     }
-  }
+    if (++ps == nst) {
+      ps = 0;
+      pph ^= 1u;
+    }
+    if (++pw == NWARP) pw = 0;
+  };
+  if (lane == 0) tma::fence_proxy_async();  // earlier generic-proxy use of the ring's shared memory
+  for (int j = 0; j < LA; ++j) produce();
   __syncwarp();
-  int ci = 0;
-  Region Cur = get(0);
-  int ck = Cur.kb;
-  Frags<NF> fr;
-  frags_for<NF>(Cur, fr);
-  double acc[NF][2];
+  int cs = r.cs;
+  unsigned cph = r.cph;
+  for (int ci = 0; ci < n; ++ci) {
+    const Region Cur = get(ci);
+    Frags<NF> fr;
+    frags_for<NF>(Cur, fr);
+    double acc[NF][2];
 #pragma unroll
-  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
-  unsigned slot = first;
-  while (ci < n) {
-    if (threadIdx.x == 0 && pi < n) {
-      issue(r, produced++, bx, P, pk);
-      if (++pk >= P.ke && ++pi < n) {
-        P = get(pi);
-        pk = P.kb;
+    for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+    Operands<NF, DEDUPE> o;
+    // region prologue: the operands of its first k-step
+    tma::mbar_wait(&r.full[cs], cph);
+    if (tl && ci == 0) r.dbg[4 * r.dbg_slot] += fb_clock() - t_start;
+    load_step<NF, DEDUPE>(r, cs, 0, bx, fr, o);
+    for (int ck = Cur.kb; ck + 1 < Cur.ke; ++ck) {
+      produce();
+      __syncwarp();
+      step<NF, DEDUPE, true>(r, cs, 0, cs, 1, bx, fr, o, acc);
+      step<NF, DEDUPE, true>(r, cs, 1, cs, 2, bx, fr, o, acc);
+      step<NF, DEDUPE, true>(r, cs, 2, cs, 3, bx, fr, o, acc);
+      int ns = cs + 1;
+      if (ns == nst) {
+        ns = 0;
+        cph ^= 1u;
+      }
+      // the last k-step loads from the next k-tile: pass its full barrier now
+      tma::mbar_wait(&r.full[ns], cph);
+      step<NF, DEDUPE, true>(r, cs, 3, ns, 0, bx, fr, o, acc);
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&r.empty[cs]);
+      cs = ns;
+    }
+    {  // the region's last k-tile
+      produce();
+      __syncwarp();
+      step<NF, DEDUPE, true>(r, cs, 0, cs, 1, bx, fr, o, acc);
+      step<NF, DEDUPE, true>(r, cs, 1, cs, 2, bx, fr, o, acc);
+      step<NF, DEDUPE, true>(r, cs, 2, cs, 3, bx, fr, o, acc);
+      step<NF, DEDUPE, false>(r, cs, 3, cs, 0, bx, fr, o, acc);
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&r.empty[cs]);
+      if (++cs == nst) {
+        cs = 0;
+        cph ^= 1u;
       }
     }
-    __syncwarp();
-    const unsigned st = slot % STAGES;
-    tma::mbar_wait(&r.full[st], (slot / STAGES) & 1u);
-    compute<NF, DEDUPE>(r, slot, bx, fr, acc);
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&r.empty[st]);
-    ++slot;
-    if (++ck >= Cur.ke) {
-      if (tl) r.dbg[4 * r.dbg_slot + 1] += fb_clock() - t_start;
-      epi(Cur, fr, acc);
-      if (tl) r.dbg[4 * r.dbg_slot + 2] += fb_clock() - t_start;
-#pragma unroll
-      for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
-      if (++ci < n) {
-        Cur = get(ci);
-        ck = Cur.kb;
-        frags_for<NF>(Cur, fr);
-      }
-    }
+    if (tl) r.dbg[4 * r.dbg_slot + 1] += fb_clock() - t_start;
+    epi(Cur, fr, acc);
+    if (tl) r.dbg[4 * r.dbg_slot + 2] += fb_clock() - t_start;
   }
   __syncthreads();
   if (tl) r.dbg[4 * r.dbg_slot + 3] += fb_clock() - t_start;
-  r.uses = slot;
+  r.cs = cs;
+  r.cph = cph;
 }
 
 // Store this warp's fragments of region g (limits M, N): rowptr(row) -> column 0 of row.

@@ -166,7 +166,7 @@ template <int NF, bool DD>
 __global__ void __launch_bounds__(384, 1) bench_fb_kernel(const __grid_constant__ TmaMaps maps, double* C, int M,
                                                            int N, int K, int items, int rb, int cb, int stride) {
   extern __shared__ unsigned char smem_raw[];
-  tmafb::Ring ring = tmafb::ring_init(smem_raw, stride, tmafb::STAGES);
+  tmafb::Ring ring = tmafb::ring_init(smem_raw, stride, 6);
   const int FR = (M + 7) / 8, FC = (N + 7) / 8;
   const int nrb = (FR + rb - 1) / rb, ncb = (FC + cb - 1) / cb;
   const int KT = (K + 15) / 16;
@@ -195,7 +195,7 @@ void run_fb(int M, int N, int K, int rb, int cb, int items, double* A, double* B
   make_tensor_map_2d(&maps.a, A, M, K, K, rb * 8);
   make_tensor_map_2d(&maps.b, B, N, K, K, cb * 8);
   const int stride = (((rb + cb) * 8 * 128 + 1023) / 1024) * 1024;
-  const size_t smem = (size_t)4 * stride + 64 + 1024 + 4096;
+  const size_t smem = (size_t)6 * stride + tmafb::HEADER + 1024 + 4096;
   cudaFuncSetAttribute(bench_fb_kernel<NF, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
