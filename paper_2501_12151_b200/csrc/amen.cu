@@ -363,6 +363,7 @@ DBuf solve_local_system(Ctx& c_, const LocalSystem& L, const double* rhs_p, cons
     a.box1_a = pl.box1_a; a.box1_b = pl.box1_b; a.box2_a = pl.box2_a; a.box2_b = pl.box2_b;
     a.stage_stride = pl.stage_stride;
     a.stages = pl.stages;
+    a.p1_frun = pl.p1_frun;
     a.b = bT.p; a.invd = dT.p; a.x = xT.p; a.r = r.p; a.z = z.p; a.p = p.p; a.q = q.p;
     a.t2 = t2.p; a.part3 = part3.p; a.S3 = pl.S3; a.kt_per3 = pl.kt_per3; a.red = red.p;
     a.dim = dim; a.atol = atol; a.maxiter = prm_.local_iter_cap; a.xany = xany ? 1 : 0;

@@ -107,8 +107,13 @@ __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy
   do {                                                                           \
     if (dedupe) {                                                                \
       switch (nf) {                                                              \
+        case 1: ring = FN<1, true>(__VA_ARGS__); break;                     \
+        case 2: ring = FN<2, true>(__VA_ARGS__); break;                     \
+        case 3: ring = FN<3, true>(__VA_ARGS__); break;                     \
         case 4: ring = FN<4, true>(__VA_ARGS__); break;                     \
+        case 5: ring = FN<5, true>(__VA_ARGS__); break;                     \
         case 6: ring = FN<6, true>(__VA_ARGS__); break;                     \
+        case 7: ring = FN<7, true>(__VA_ARGS__); break;                     \
         case 8: ring = FN<8, true>(__VA_ARGS__); break;                     \
         case 10: ring = FN<10, true>(__VA_ARGS__); break;                   \
         case 12: ring = FN<12, true>(__VA_ARGS__); break;                   \
@@ -116,8 +121,13 @@ __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy
       }                                                                          \
     } else {                                                                     \
       switch (nf) {                                                              \
+        case 1: ring = FN<1, false>(__VA_ARGS__); break;                    \
+        case 2: ring = FN<2, false>(__VA_ARGS__); break;                    \
+        case 3: ring = FN<3, false>(__VA_ARGS__); break;                    \
         case 4: ring = FN<4, false>(__VA_ARGS__); break;                    \
+        case 5: ring = FN<5, false>(__VA_ARGS__); break;                    \
         case 6: ring = FN<6, false>(__VA_ARGS__); break;                    \
+        case 7: ring = FN<7, false>(__VA_ARGS__); break;                    \
         case 8: ring = FN<8, false>(__VA_ARGS__); break;                    \
         case 10: ring = FN<10, false>(__VA_ARGS__); break;                  \
         case 12: ring = FN<12, false>(__VA_ARGS__); break;                  \
@@ -138,15 +148,30 @@ __device__ __noinline__ tmafb::Ring phase1_t(const CGTmaArgs& a, const CUtensorM
   const int RB = a.p1_rb, CB = a.p1_cb;
   const int nrb = (r1 - r0 + RB - 1) / RB, ncb = (FC + CB - 1) / CB;
   const tmafb::Boxes bx{&a.map_bop, mv, a.box1_a, a.box1_b};
+  // p1_frun: one region per CTA, its exact 1/G share of ALL fragments (row-major run)
+  const long long Fall = (long long)FR * FC;
+  const int fb_all = (int)(Fall * c / G), fe_all = (int)(Fall * (c + 1) / G);
   auto get = [&](int i) {
-    const int rb = i / ncb, cb = i - (i / ncb) * ncb;
     tmafb::Region g;
+    g.kb = 0;
+    g.ke = KT;
+    if (a.p1_frun) {
+      const int fr0 = fb_all / FC, fr1 = (fe_all - 1) / FC + 1;
+      g.m0 = fr0 * 8;
+      g.mrows = (fr1 - fr0) * 8;
+      g.n0 = 0;
+      g.ncols = FC * 8;
+      g.fb = fb_all - fr0 * FC;
+      g.fe = fe_all - fr0 * FC;
+      return g;
+    }
+    const int rb = i / ncb, cb = i - (i / ncb) * ncb;
     g.m0 = (r0 + rb * RB) * 8;
     g.mrows = min(RB, r1 - r0 - rb * RB) * 8;
     g.n0 = cb * CB * 8;
     g.ncols = min(CB, FC - cb * CB) * 8;
-    g.kb = 0;
-    g.ke = KT;
+    g.fb = 0;
+    g.fe = 0;
     return g;
   };
   const int R1 = a.R1, rk = a.rk;
@@ -158,7 +183,8 @@ __device__ __noinline__ tmafb::Ring phase1_t(const CGTmaArgs& a, const CUtensorM
       return t2 + xm * K3p + (long long)bb * rk;
     });
   };
-  tmafb::stream<NF, DEDUPE>(ring, bx, r1 > r0 ? nrb * ncb : 0, get, epi);
+  const int nreg = a.p1_frun ? (fe_all > fb_all ? 1 : 0) : (r1 > r0 ? nrb * ncb : 0);
+  tmafb::stream<NF, DEDUPE>(ring, bx, nreg, get, epi);
   return ring;
 }
 
@@ -190,6 +216,8 @@ __device__ __noinline__ tmafb::Ring phase2_t(const CGTmaArgs& a, tmafb::Ring rin
     g.ncols = min(CB, FC - tc * CB) * 8;
     g.kb = s * ktp;
     g.ke = min(KT, g.kb + ktp);
+    g.fb = 0;
+    g.fe = 0;
     return g;
   };
   const long long dim = a.dim;
@@ -457,7 +485,28 @@ CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int 
   // dedupe needs every column block (the last may be narrower) to hold a run in 2 rows
   const int cb1_min = FC1 % p.p1_cb == 0 ? p.p1_cb : FC1 % p.p1_cb;
   p.p1_dedupe = tmafb::dedupe_ok(p.p1_nf, cb1_min) ? 1 : 0;
-  if (const char* e = std::getenv("QTT_TMA_DEDUPE")) p.p1_dedupe = p.p1_dedupe && std::atoi(e);
+  // fragment-run dealing: when one region per CTA can hold its 1/G share of all fragments
+  // (all columns in one box), CTAs get equal fragment counts instead of whole fragment rows
+  p.p1_frun = 0;
+  {
+    const long long Fall = (long long)FR1 * FC1;
+    int fmax = 0, rmax = 1;
+    for (int c = 0; c < grid; ++c) {
+      const int fb = (int)(Fall * c / grid), fe = (int)(Fall * (c + 1) / grid);
+      if (fe <= fb) continue;
+      fmax = std::max(fmax, fe - fb);
+      rmax = std::max(rmax, (fe - 1) / FC1 - fb / FC1 + 1);
+    }
+    static const int frun_env = std::getenv("QTT_TMA_FRUN") ? std::atoi(std::getenv("QTT_TMA_FRUN")) : 1;
+    if (frun_env && FC1 <= 32 && fmax > 0 && fmax <= FMAX && rmax <= 32 && (rmax + FC1) * 8 * 128 <= 48 * 1024) {
+      p.p1_frun = 1;
+      p.p1_cb = FC1;
+      p.box1_a = rmax * 8;
+      p.box1_b = FC1 * 8;
+      p.p1_nf = tmafb::nf_for(fmax);
+      p.p1_dedupe = tmafb::dedupe_ok(p.p1_nf, FC1) ? 1 : 0;
+    }
+  }
   // phase 2: split-K; choose the fragment-block tiling and split count that
   // minimise per-CTA DMMAs plus the split-K partial traffic
   const int FR3 = cdiv(rb, 8), FC3 = cdiv(lb * m, 8);
@@ -481,7 +530,11 @@ CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int 
       // (the latency term keeps the 4-stage ring's value: the split it selects fixes the
       // summation order of q, and with it the solve's trajectory)
       const int nst = 4;
-      const double per_kt = std::max({(double)tmafb::nf_for(RB * CB) * 4.0 * 48.0, (RB + CB) * 8.0 * 128.0 / 24.0,
+      // (the model keeps the even fragment counts it was tuned with: its choice of split fixes
+      // the summation order of q)
+      const int per12 = cdiv(RB * CB, tmafb::NWARP);
+      const int nf_model = per12 <= 4 ? 4 : per12 <= 6 ? 6 : per12 <= 8 ? 8 : per12 <= 10 ? 10 : per12 <= 12 ? 12 : 16;
+      const double per_kt = std::max({(double)nf_model * 4.0 * 48.0, (RB + CB) * 8.0 * 128.0 / 24.0,
                                       4000.0 / (nst - 1)});
       const double dmma = per_kt * ktp;
       const double traffic = (double)S * rb * lb * m * 8.0 * 2.0 / 4.0e12 * 1.965e9;  // write+read at ~4 TB/s

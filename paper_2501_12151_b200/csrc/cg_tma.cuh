@@ -21,6 +21,7 @@ struct CGTmaArgs {
   int p1_rb, p1_cb, p2_rb, p2_cb;  // fragment-block sizes of the phase regions (cg_tma_plan)
   int p1_nf, p1_dedupe, p2_nf, p2_dedupe;
   int box1_a, box1_b, box2_a, box2_b;
+  int p1_frun;       // phase 1: fragment-run dealing (one region per CTA, equal fragment counts)
   int stage_stride;  // ring bytes per stage
   int stages;        // ring depth
   const double* b;     // rhs^T
@@ -46,7 +47,7 @@ struct CGTmaPlan {
   int p1_rb, p1_cb, p2_rb, p2_cb, S3, kt_per3;
   int p1_nf, p1_dedupe, p2_nf, p2_dedupe;
   int box1_a, box1_b, box2_a, box2_b;  // TMA box rows per operand
-  int stage_stride, stages;
+  int stage_stride, stages, p1_frun;
 };
 
 bool cg_tma_supported(int lk, int n);

@@ -25,9 +25,10 @@ constexpr int NWARP = 12;  // consumer warps per CTA: 3 per scheduler
 constexpr int MAX_STAGES = 8;  // deepest ring (run-time depth Ring::nst; look-ahead nst - 2 k-tiles)
 constexpr int HEADER = 256;    // mbarriers (full + empty per stage) before the ring
 
-// One unit of work: output rows [m0, m0+mrows) x cols [n0, n0+ncols), k-tiles [kb, ke).
+// One unit of work: fragments [fb, fe) (row-major numbering) of the fragment grid covering
+// output rows [m0, m0+mrows) x cols [n0, n0+ncols), over k-tiles [kb, ke).  fe = 0: the whole grid.
 struct Region {
-  int m0, mrows, n0, ncols, kb, ke;
+  int m0, mrows, n0, ncols, kb, ke, fb, fe;
 };
 
 struct Ring {
@@ -98,16 +99,19 @@ template <int NF>
 struct Frags {
   int t1;          // first fragment of the second row (NF if none)
   unsigned valid;  // bit f: fragment f inside the region
-  int boff[NF];    // B fragment row offset in the stage (doubles, incl. lane row)
-  int aoff[NF];    // A fragment row offset (doubles, incl. lane row)
+  int boff[NF];    // B fragment row offset in the stage (BYTES, incl. lane row)
+  int aoff[NF];    // A fragment row offset (BYTES, incl. lane row)
+  int ko[4];       // byte offset of this lane's 8-byte element in k-step 0..3 (128B swizzle)
 };
 
 template <int NF>
 __device__ __forceinline__ void frags_for(const Region& g, Frags<NF>& fr) {
   const int FN = (g.ncols + 7) >> 3, FM = (g.mrows + 7) >> 3;
-  const int F = FM * FN;
+  const int F = g.fe > 0 ? g.fe : FM * FN;
   const int warp = threadIdx.x >> 5, lr = (threadIdx.x & 31) >> 2;
-  const int g0 = warp * NF;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) fr.ko[ks] = tma::swz_off(ks, lr, threadIdx.x & 3) * 8;
+  const int g0 = g.fb + warp * NF;
   // a warp past the region keeps row/col 0 for its (dropped) fragments: all of its
   // shared-memory reads stay inside the stage
   const int i0 = g0 < F ? g0 / FN : 0;
@@ -120,8 +124,8 @@ __device__ __forceinline__ void frags_for(const Region& g, Frags<NF>& fr) {
     if (ok) fr.valid |= 1u << f;
     if (i != i0 && fr.t1 == NF) fr.t1 = f;
     const int ii = ok ? i : i0, jj = ok ? j : 0;  // dropped fragments read row/col 0 of the run
-    fr.aoff[f] = (ii * 8 + lr) * 16;
-    fr.boff[f] = (jj * 8 + lr) * 16;
+    fr.aoff[f] = (ii * 8 + lr) * 128;
+    fr.boff[f] = (jj * 8 + lr) * 128;
     if (++j == FN) {
       j = 0;
       ++i;
@@ -140,18 +144,16 @@ struct Operands {
 template <int NF, bool DEDUPE>
 __device__ __forceinline__ void load_step(const Ring& r, int s, int ks, const Boxes& bx, const Frags<NF>& fr,
                                           Operands<NF, DEDUPE>& o) {
-  const unsigned sA = tma::smem_u32(r.base) + s * r.stride;
+  const unsigned sA = tma::smem_u32(r.base) + s * r.stride + fr.ko[ks];
   const unsigned sB = sA + bx.box_a * 128;
-  const int lane = threadIdx.x & 31;
-  const int off = tma::swz_off(ks, lane >> 2, lane & 3);
   if constexpr (DEDUPE) {
-    o.a[0] = tma::lds64(sA + (fr.aoff[0] + off) * 8);
-    o.a[1] = tma::lds64(sA + (fr.aoff[0] + 128 + off) * 8);
+    o.a[0] = tma::lds64(sA + fr.aoff[0]);
+    o.a[1] = tma::lds64(sA + fr.aoff[0] + 1024);
   } else {
-    o.a[0] = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+    o.a[0] = tma::lds64(sA + fr.aoff[0]);
   }
 #pragma unroll
-  for (int f = 0; f < NF; ++f) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+  for (int f = 0; f < NF; ++f) o.b[f] = tma::lds64(sB + fr.boff[f]);
 }
 
 // Issue the DMMAs of the k-step held in o and, when NEXT, replace every operand by that of
@@ -162,20 +164,18 @@ __device__ __forceinline__ void load_step(const Ring& r, int s, int ks, const Bo
 template <int NF, bool DEDUPE, bool NEXT>
 __device__ __forceinline__ void step(const Ring& r, int s_c, int ks_c, int s_n, int ks_n, const Boxes& bx,
                                      const Frags<NF>& fr, Operands<NF, DEDUPE>& o, double (&acc)[NF][2]) {
-  const unsigned sA = tma::smem_u32(r.base) + s_n * r.stride;
+  const unsigned sA = tma::smem_u32(r.base) + s_n * r.stride + fr.ko[ks_n];
   const unsigned sB = sA + bx.box_a * 128;
-  const int lane = threadIdx.x & 31;
-  const int off = tma::swz_off(ks_n, lane >> 2, lane & 3);
   if constexpr (DEDUPE) {
     double n0 = 0.0, n1 = 0.0;
     if constexpr (NEXT) {
-      n0 = tma::lds64(sA + (fr.aoff[0] + off) * 8);
-      n1 = tma::lds64(sA + (fr.aoff[0] + 128 + off) * 8);
+      n0 = tma::lds64(sA + fr.aoff[0]);
+      n1 = tma::lds64(sA + fr.aoff[0] + 1024);
     }
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       tile::dmma(acc[f], f < fr.t1 ? o.a[0] : o.a[1], o.b[f]);
-      if constexpr (NEXT) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+      if constexpr (NEXT) o.b[f] = tma::lds64(sB + fr.boff[f]);
     }
     if constexpr (NEXT) {
       o.a[0] = n0;
@@ -183,18 +183,17 @@ __device__ __forceinline__ void step(const Ring& r, int s_c, int ks_c, int s_n, 
     }
   } else {
     // A fragments one ahead of their DMMA (this step's from the current stage s_c)
-    const unsigned sAc = tma::smem_u32(r.base) + s_c * r.stride;
-    const int offc = tma::swz_off(ks_c, lane >> 2, lane & 3);
+    const unsigned sAc = tma::smem_u32(r.base) + s_c * r.stride + fr.ko[ks_c];
     double a = o.a[0];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       double an = 0.0;
       if (f + 1 < NF)
-        an = tma::lds64(sAc + (fr.aoff[f + 1] + offc) * 8);
+        an = tma::lds64(sAc + fr.aoff[f + 1]);
       else if constexpr (NEXT)
-        an = tma::lds64(sA + (fr.aoff[0] + off) * 8);
+        an = tma::lds64(sA + fr.aoff[0]);
       tile::dmma(acc[f], a, o.b[f]);
-      if constexpr (NEXT) o.b[f] = tma::lds64(sB + (fr.boff[f] + off) * 8);
+      if constexpr (NEXT) o.b[f] = tma::lds64(sB + fr.boff[f]);
       a = an;
     }
     o.a[0] = a;
@@ -304,8 +303,8 @@ __device__ __forceinline__ void store(const Region& g, const Frags<NF>& fr, cons
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     if (fr.valid & (1u << f)) {
-      const int row = g.m0 + fr.aoff[f] / 16;
-      const int col = g.n0 + (fr.boff[f] / 16 - lr) + lc * 2;
+      const int row = g.m0 + fr.aoff[f] / 128;
+      const int col = g.n0 + (fr.boff[f] / 128 - lr) + lc * 2;
       if (row < rlim) {
         double* dst = rowptr(row);
         if (col + 1 < clim) {
@@ -322,7 +321,7 @@ __device__ __forceinline__ void store(const Region& g, const Frags<NF>& fr, cons
 // Fragments per warp for a region of F fragments (instantiated sizes).
 __host__ __device__ inline int nf_for(int F) {
   const int per = (F + NWARP - 1) / NWARP;
-  return per <= 4 ? 4 : per <= 6 ? 6 : per <= 8 ? 8 : per <= 10 ? 10 : per <= 12 ? 12 : 16;
+  return per <= 1 ? 1 : per <= 8 ? per : per <= 10 ? 10 : per <= 12 ? 12 : 16;
 }
 // A warp run of nf fragments over rows of fn fragments spans at most 2 rows.
 __host__ __device__ inline bool dedupe_ok(int nf, int fn) { return nf <= fn + 1; }

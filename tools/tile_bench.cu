@@ -350,7 +350,7 @@ int main() {
   if (getenv("TB_FB16")) {
     double *A, *B, *C;
     cudaMalloc(&A, (size_t)10400 * 1600 * 8);
-    cudaMalloc(&B, (size_t)1600 * 112 * 8);
+    cudaMalloc(&B, (size_t)1600 * 256 * 8);
     cudaMalloc(&C, (size_t)10400 * 112 * 8);
     const int v = atoi(getenv("TB_FB16"));
     if (v == 1) run_fb<16, false>(10400, 100, 200, 9, 13, 1, A, B, C);
@@ -362,6 +362,20 @@ int main() {
     if (v == 7) run_fb<10, false>(10400, 100, 200, 9, 13, 8, A, B, C);
     if (v == 8) run_fb<10, true>(10400, 100, 1600, 9, 13, 1, A, B, C);
     if (v == 9) run_fb<8, true>(10400, 100, 1600, 8, 12, 1, A, B, C);
+    if (v == 11) {
+      run_fb<10, true>(10400, 100, 1600, 9, 13, 1, A, B, C);
+      run_fb<10, false>(10400, 100, 1600, 9, 13, 1, A, B, C);
+      run_fb<8, true>(10400, 100, 1600, 7, 13, 1, A, B, C);
+      run_fb<8, false>(10400, 100, 1600, 7, 13, 1, A, B, C);
+      run_fb<6, true>(10400, 100, 1600, 5, 13, 1, A, B, C);
+      run_fb<6, false>(10400, 100, 1600, 5, 13, 1, A, B, C);
+      run_fb<4, true>(10400, 100, 1600, 3, 13, 1, A, B, C);
+      run_fb<4, false>(10400, 100, 1600, 3, 13, 1, A, B, C);
+      run_fb<6, false>(1040, 200, 1600, 13, 5, 1, A, B, C);
+      run_fb<8, false>(1040, 200, 1600, 13, 7, 1, A, B, C);
+      run_fb<12, true>(10400, 100, 1600, 11, 13, 1, A, B, C);
+      run_fb<16, false>(10400, 100, 1600, 14, 13, 1, A, B, C);
+    }
     printf("v=%d %s\n", v, cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
   }
