@@ -49,8 +49,8 @@ def fp64_peak():
 
 def k1_traffic():
     """DRAM bytes per K1 call inside the CG kernel, from the committed ncu --set full capture
-    (profiles/r01/cg_tma_traffic.json; the operands stay L2-resident across iterations)."""
-    p = os.path.join(ROOT, "profiles", "r01", "cg_tma_traffic.json")
+    (profiles/r02/cg_tma_traffic.json; the operands stay L2-resident across iterations)."""
+    p = os.path.join(ROOT, "profiles", "r02", "cg_tma_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
