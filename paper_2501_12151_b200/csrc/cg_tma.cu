@@ -447,9 +447,12 @@ constexpr size_t SMEM_MAX = 224 * 1024;  // + static shared memory <= the 227 KB
 size_t cg_tma_smem(int stride, int nst) {
   return std::max((size_t)nst * stride, (size_t)NW * NTC * sizeof(double)) + tmafb::HEADER + 1024 + 4096;
 }
-// Ring depth: 6 stages (look-ahead 4 k-tiles) when they fit, at least 3 (QTT_TMA_STAGES overrides)
+// Ring depth: 4 stages (look-ahead 2 k-tiles) when they fit, at least 3 (QTT_TMA_STAGES
+// overrides).  Measured at r = 100, R = 31 / 52 (both GEMM phases of one matvec, us): 3 stages
+// 18.96 / 29.46, 4 stages 18.63 / 29.05, 6 stages 18.98 / 29.46, 8 stages 19.23 / 29.81 -- a
+// deeper prologue burst only delays the first k-tile (phase 2 first data 1.5 -> 2.9 us).
 int cg_tma_stages(int stride) {
-  int want = 6;
+  int want = 4;
   if (const char* e = std::getenv("QTT_TMA_STAGES")) want = std::atoi(e);
   const int fit = (int)((SMEM_MAX - tmafb::HEADER - 1024 - 4096) / (size_t)stride);
   return std::max(3, std::min({want, fit, tmafb::MAX_STAGES}));

@@ -21,7 +21,7 @@ namespace qtt {
 namespace tmafb {
 
 constexpr int MAXF = 16;   // fragments per warp (largest instantiation)
-constexpr int NWARP = 12;  // consumer warps per CTA: 3 per scheduler
+constexpr int NWARP = 12;  // consumer warps per CTA: 3 per scheduler (16 warps at 128 registers: no faster)
 constexpr int MAX_STAGES = 8;  // deepest ring (run-time depth Ring::nst; look-ahead nst - 2 k-tiles)
 constexpr int HEADER = 256;    // mbarriers (full + empty per stage) before the ring
 
@@ -85,9 +85,14 @@ struct Boxes {
 __device__ __forceinline__ void issue(Ring& r, int s, unsigned ph, const Boxes& bx, const Region& g, int kt) {
   tma::mbar_wait(&r.empty[s], ph ^ 1u);
   unsigned char* st = r.base + (size_t)s * r.stride;
+#ifdef QTT_FB_NOLOAD  // tools/tile_bench.cu: the loop without the TMA copies (stale operands)
+  tma::mbar_arrive(&r.full[s]);
+  (void)st;
+#else
   tma::mbar_expect_tx(&r.full[s], (bx.box_a + bx.box_b) * 128);
   tma::load_2d(st, bx.ma, kt * 16, g.m0, &r.full[s]);
   tma::load_2d(st + bx.box_a * 128, bx.mb, kt * 16, g.n0, &r.full[s]);
+#endif
 }
 
 // This warp's fragment run inside a region: fragments g0 .. g0+NF-1 of the

@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(384, 1) bench_fb_kernel(const __grid_constant_
     g.ncols = min(cb, FC - c * cb) * 8;
     g.kb = 0;
     g.ke = KT;
+    g.fb = 0;
+    g.fe = 0;
     return g;
   };
   auto epi = [&](const tmafb::Region& g, const auto& fr, const auto& acc) {
