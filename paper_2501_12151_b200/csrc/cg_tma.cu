@@ -2,8 +2,8 @@
 // local matvec runs on the TMA tile engine (tma_tile.cuh).  Per iteration:
 //   phase 1  t2[(X,m,b),V] = sum_(U,n) Bop[(X,m,b),(U,n)] p^T[V,(U,n)]
 //            (Bop = left environment composed with the operator core, built once per
-//            solve; one GEMM over all X, every CTA an exact 1/148 share of the output,
-//            DMMA fragments dealt evenly to its warps -- tma_fb.cuh)
+//            solve; one GEMM over all X, every CTA an exact 1/148 share of the output
+//            fragments, dealt evenly to its warps -- tma_fb.cuh)
 //   phase 2  q^T[Y,(X,m)] = sum_(b,V) phir[Y,(b,V)] t2[(X,m),(b,V)]   (split-K)
 //   then the split-K reduction + p.q, the x/r/z update + r.r, r.z, and p = z + beta p,
 // phases separated by grid barriers, everything resident in L2/HBM between them.

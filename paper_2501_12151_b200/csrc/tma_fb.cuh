@@ -4,16 +4,18 @@
 // 100) are too small for fixed CTA tiles: rounding the tile count to the 148 SMs,
 // and the warp count of a tile to the 4 schedulers per SM, idles up to half of the
 // DMMA pipes (tools/tile_bench.cu).  Here each CTA gets an output REGION sized to
-// its exact share of the work (a run of 8-row fragment rows, all columns, or a
-// column block), and inside the region the 8x8 DMMA fragments are dealt out to the
-// 12 warps (3 per scheduler) in equal contiguous runs (row-major), so every
-// scheduler issues the same number of DMMAs.  A warp keeps up to MAXF fragment
-// accumulators; when its run spans at most 2 fragment rows the A fragments are
-// loaded once per row and picked with a predicated select.
+// its exact share of the work -- a run of 8x8 DMMA fragments of the row-major fragment
+// grid (Region::fb, fe), or whole fragment rows / a column block -- and inside the
+// region the fragments are dealt out to the 12 warps (3 per scheduler) in equal
+// contiguous runs, so every scheduler issues the same number of DMMAs.  A warp keeps
+// up to MAXF fragment accumulators; when its run spans at most 2 fragment rows the A
+// fragments are loaded once per row and picked with a select.
 //
 // Operands are K-contiguous (C = A . B^T); per k-tile one TMA box of A rows and one
-// of B rows (16 doubles of K each, 128B swizzle) land in a 4-stage ring guarded by
-// full/empty mbarriers; thread 0 produces.
+// of B rows (16 doubles of K each, 128B swizzle) land in a ring of run-time depth
+// guarded by full/empty mbarriers.  The consumer loop is software-pipelined (the
+// operands of the next k-step, also across a k-tile boundary, are loaded while the
+// current k-step's DMMAs issue) and the TMA issue rotates over the warps (stream()).
 #pragma once
 #include "tma_tile.cuh"
 
@@ -313,8 +315,12 @@ __device__ __forceinline__ void store(const Region& g, const Frags<NF>& fr, cons
       if (row < rlim) {
         double* dst = rowptr(row);
         if (col + 1 < clim) {
-          dst[col] = acc[f][0];
-          dst[col + 1] = acc[f][1];
+          if ((reinterpret_cast<uintptr_t>(dst + col) & 15) == 0) {
+            *reinterpret_cast<double2*>(dst + col) = make_double2(acc[f][0], acc[f][1]);
+          } else {
+            dst[col] = acc[f][0];
+            dst[col + 1] = acc[f][1];
+          }
         } else if (col < clim) {
           dst[col] = acc[f][0];
         }
