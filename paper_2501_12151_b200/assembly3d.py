@@ -175,23 +175,36 @@ def _op_sum(trains):
         for t in trains[1:]:
             acc = acc + t[0]
         return [acc]
-    out = []
+    # all cores live back to back in ONE buffer: DeviceTrain.upload then sends it as it is
+    # (the 21-term C3 sum is 1.45 GB; gathering its cores into an upload buffer cost 0.3 s)
+    shapes = []
     for k in range(K):
         cs = [t[k] for t in trains]
         if k == 0:
-            out.append(np.concatenate(cs, axis=3))
+            shapes.append((1, cs[0].shape[1], cs[0].shape[2], sum(c.shape[3] for c in cs)))
         elif k == K - 1:
-            out.append(np.concatenate(cs, axis=0))
+            shapes.append((sum(c.shape[0] for c in cs), cs[0].shape[1], cs[0].shape[2], 1))
         else:
-            r0 = sum(c.shape[0] for c in cs)
-            r1 = sum(c.shape[3] for c in cs)
-            c = np.zeros((r0, cs[0].shape[1], cs[0].shape[2], r1))
-            i = j = 0
-            for b in cs:
+            shapes.append((sum(c.shape[0] for c in cs), cs[0].shape[1], cs[0].shape[2],
+                           sum(c.shape[3] for c in cs)))
+    flat = np.zeros(sum(int(np.prod(sh)) for sh in shapes))
+    out, off = [], 0
+    for k, sh in enumerate(shapes):
+        n = int(np.prod(sh))
+        c = flat[off:off + n].reshape(sh)
+        off += n
+        i = j = 0
+        for t in trains:
+            b = t[k]
+            if k == 0:
+                c[:, :, :, j:j + b.shape[3]] = b
+            elif k == K - 1:
+                c[i:i + b.shape[0]] = b
+            else:
                 c[i:i + b.shape[0], :, :, j:j + b.shape[3]] = b
-                i += b.shape[0]
-                j += b.shape[3]
-            out.append(c)
+            i += b.shape[0]
+            j += b.shape[3]
+        out.append(c)
     return out
 
 
