@@ -5,9 +5,14 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "gemm.cuh"
 #include "linalg.cuh"
 #include "svd_block.cuh"
+#include "tma_tile.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace qtt {
 namespace {
@@ -735,6 +740,264 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
   }
 }
 
+// ---- the same square one-sided Jacobi on a 2-CTA cluster: CTA 0 holds W, finds the angles and
+// rotates W; CTA 1 holds V and applies the same rotations one hop behind.  The dependency is
+// one-way (V never feeds an angle), so the DSMEM hop is a pipeline delay, not a per-round round
+// trip (the row-split cluster variants measured earlier paid one per round).  Each CTA moves half
+// of the shared-memory traffic that bounds the single-CTA kernel.  Per round CTA 0's group
+// leaders store (cs, sn) into a ring slot of CTA 1's shared memory, thread 0 then arrives
+// (release.cluster) on that slot's mbarrier in CTA 1; CTA 1 hands the slot back through an
+// mbarrier in CTA 0.  After the last sweep CTA 0 sends the column ranks with a STOP header.
+// Every floating-point operation and its order are those of jacobi_sq_kernel: same bits.
+namespace jq2 {
+constexpr int DEPTH = 8;     // ring slots
+constexpr int MAXG = 64;     // rotation groups per round (<= 56)
+struct Mail {                // lives in CTA 1's shared memory (CTA 0 writes it remotely)
+  double cs[DEPTH][MAXG];
+  double sn[DEPTH][MAXG];
+  int hdr[DEPTH];            // 0: a round's rotations, 1: stop (rank[] is valid)
+  int rank[128];
+};
+__device__ __forceinline__ unsigned map_remote(const void* p, unsigned cta) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void remote_arrive(unsigned remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void st_remote_f64(unsigned addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote_s32(unsigned addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+}  // namespace jq2
+
+template <int NT, int K>
+__global__ void __launch_bounds__(NT) jacobi_sq2_kernel(CMatView in, MatView Uo, double* so, MatView Vto,
+                                                        double tol, int dbg) {
+  constexpr int GS = 8, SEG = 16 * K;
+  extern __shared__ double sm[];
+  __shared__ int s_rot[2];
+  __shared__ jq2::Mail mail;                       // used in CTA 1
+  __shared__ __align__(8) uint64_t full[jq2::DEPTH];   // used in CTA 1: slot filled by CTA 0
+  __shared__ __align__(8) uint64_t empty[jq2::DEPTH];  // used in CTA 0: slot released by CTA 1
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank_in_cl = cl.block_rank();
+  const int n = in.cols;
+  double* S = sm;  // n columns of SEG doubles: W in CTA 0, V in CTA 1
+  double* sig = S + (long long)SEG * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  const int gl = tid % GS, grp = tid / GS;
+  const double tol2 = tol * tol;
+  if (tid == 0) {
+    for (int i = 0; i < jq2::DEPTH; ++i) {
+      tma::mbar_init(&full[i], 1);
+      tma::mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int e = tid; e < SEG * n; e += NT) {
+    const int i = e % SEG, j = e / SEG;
+    double v = 0.0;
+    if (rank_in_cl == 0) {
+      if (i < n) v = in.p[i * in.rs + j * in.cs];
+    } else if (i == j) {
+      v = 1.0;
+    }
+    S[e] = v;
+  }
+  cl.sync();
+  const int P = n + (n & 1), half = P / 2;
+  const bool warp_live = warp * (32 / GS) < half;
+  auto pair_of = [&](int r, int& a, int& b) {
+    const int q = grp;
+    if (q == 0) { a = r; b = P - 1; }
+    else { a = (r + q) % (P - 1); b = (r - q + (P - 1)) % (P - 1); }
+    const bool live = q < half && a < n && b < n;
+    if (a > b) { const int t = a; a = b; b = t; }
+    if (!live) { a = 0; b = 0; }
+    return live;
+  };
+  if (rank_in_cl == 0) {
+    // ---------------- CTA 0: W, the angles, the convergence decision
+    const unsigned r_cs = jq2::map_remote(&mail.cs[0][0], 1), r_sn = jq2::map_remote(&mail.sn[0][0], 1);
+    const unsigned r_hdr = jq2::map_remote(&mail.hdr[0], 1), r_rank = jq2::map_remote(&mail.rank[0], 1);
+    const unsigned r_full = jq2::map_remote(&full[0], 1);
+    unsigned t = 0;  // rounds sent so far
+    int sweeps_done = 0;
+    for (int sweep = 0; sweep < 80; ++sweep) {
+      if (tid == 0) s_rot[sweep & 1] = 0;
+      __syncthreads();
+      int rotated = 0;
+      for (int r = 0; r < P - 1; ++r, ++t) {
+        const unsigned slot = t % jq2::DEPTH;
+        if (warp_live) {
+          int a, b;
+          const bool live = pair_of(r, a, b);
+          double2* wa = reinterpret_cast<double2*>(S + (long long)a * SEG) + gl;
+          double2* wb = reinterpret_cast<double2*>(S + (long long)b * SEG) + gl;
+          double2 x[K], y[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            x[k] = wa[k * GS];
+            y[k] = wb[k * GS];
+          }
+          double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            al0 = fma(x[k].x, x[k].x, al0); be0 = fma(y[k].x, y[k].x, be0); ga0 = fma(x[k].x, y[k].x, ga0);
+            al1 = fma(x[k].y, x[k].y, al1); be1 = fma(y[k].y, y[k].y, be1); ga1 = fma(x[k].y, y[k].y, ga1);
+          }
+          double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+#pragma unroll
+          for (int o = GS / 2; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          double cs = 2.0, sn = 0.0;  // cs = 2: no rotation
+          const bool rot = live && jac_angle(al, be, ga, tol2, cs, sn);
+          if (!rot) cs = 2.0;
+          if (gl == 0) {
+            if (t >= (unsigned)jq2::DEPTH) jq2::wait_cluster(&empty[slot], ((t / jq2::DEPTH) - 1) & 1u);
+            jq2::st_remote_f64(r_cs + (slot * jq2::MAXG + grp) * 8, cs);
+            jq2::st_remote_f64(r_sn + (slot * jq2::MAXG + grp) * 8, sn);
+          }
+          if (rot) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              wa[k * GS] = make_double2(cs * x[k].x - sn * y[k].x, cs * x[k].y - sn * y[k].y);
+              wb[k * GS] = make_double2(sn * x[k].x + cs * y[k].x, sn * x[k].y + cs * y[k].y);
+            }
+            rotated = 1;
+          }
+        }
+        if (tid == 0) {
+          if (t >= (unsigned)jq2::DEPTH) jq2::wait_cluster(&empty[slot], ((t / jq2::DEPTH) - 1) & 1u);
+          jq2::st_remote_s32(r_hdr + slot * 4, 0);
+        }
+        __syncthreads();
+        if (tid == 0) jq2::remote_arrive(r_full + slot * 8);
+      }
+      if (rotated) s_rot[sweep & 1] = 1;
+      __syncthreads();
+      sweeps_done = sweep + 1;
+      if (!s_rot[sweep & 1]) break;
+    }
+    if (dbg && tid == 0) printf("[qtt] jacobi(sq2) %dx%d sweeps %d\n", n, n, sweeps_done);
+    for (int c = warp; c < n; c += NW) {
+      const double* wc = S + (long long)c * SEG;
+      double s2 = 0;
+      for (int i = lane; i < n; i += 32) s2 += wc[i] * wc[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) sig[c] = sqrt(s2);
+    }
+    __syncthreads();
+    const unsigned slot = t % jq2::DEPTH;
+    if (tid == 0 && t >= (unsigned)jq2::DEPTH) jq2::wait_cluster(&empty[slot], ((t / jq2::DEPTH) - 1) & 1u);
+    __syncthreads();
+    for (int c = tid; c < n; c += NT) {
+      const double sc = sig[c];
+      int rank = 0;
+      for (int d = 0; d < n; ++d) {
+        const double sd = sig[d];
+        rank += (sd > sc) || (sd == sc && d < c);
+      }
+      jq2::st_remote_s32(r_rank + c * 4, rank);
+      so[rank] = sc;
+      const double inv = sc > 0 ? 1.0 / sc : 0.0;
+      const double* wc = S + (long long)c * SEG;
+      if (Uo.p)
+        for (int i = 0; i < n; ++i)
+          Uo.p[i * Uo.rs + rank * Uo.cs] = sc > 0 ? wc[i] * inv : (i == rank ? 1.0 : 0.0);
+    }
+    if (tid == 0) jq2::st_remote_s32(r_hdr + slot * 4, 1);
+    __syncthreads();
+    if (tid == 0) jq2::remote_arrive(r_full + slot * 8);
+  } else {
+    // ---------------- CTA 1: V, one hop behind
+    const unsigned r_empty = jq2::map_remote(&empty[0], 0);
+    unsigned t = 0;
+    for (;; ++t) {
+      const unsigned slot = t % jq2::DEPTH;
+      jq2::wait_cluster(&full[slot], (t / jq2::DEPTH) & 1u);
+      if (mail.hdr[slot] != 0) break;
+      const int r = (int)(t % (unsigned)(P - 1));
+      if (warp_live) {
+        int a, b;
+        pair_of(r, a, b);
+        const double cs = mail.cs[slot][grp], sn = mail.sn[slot][grp];
+        if (cs != 2.0) {
+          double2* wa = reinterpret_cast<double2*>(S + (long long)a * SEG) + gl;
+          double2* wb = reinterpret_cast<double2*>(S + (long long)b * SEG) + gl;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double2 u = wa[k * GS], v = wb[k * GS];
+            wa[k * GS] = make_double2(cs * u.x - sn * v.x, cs * u.y - sn * v.y);
+            wb[k * GS] = make_double2(sn * u.x + cs * v.x, sn * u.y + cs * v.y);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) jq2::remote_arrive(r_empty + slot * 8);
+    }
+    if (Vto.p)
+      for (int c = tid; c < n; c += NT) {
+        const int rank = mail.rank[c];
+        const double* vc = S + (long long)c * SEG;
+        for (int i = 0; i < n; ++i) Vto.p[rank * Vto.rs + i * Vto.cs] = vc[i];
+      }
+  }
+  cl.sync();  // neither CTA leaves while the other may still write its shared memory
+}
+
+template <int NT, int K>
+static bool jacobi_sq2_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt, double tol) {
+  static PerDevice<int> ok_dev(-1);
+  int& ok = ok_dev();
+  const size_t bytes = ((size_t)16 * K * in.cols + in.cols) * sizeof(double);
+  if (ok < 0) {
+    ok = cudaFuncSetAttribute(jacobi_sq2_kernel<NT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kSmemDoubles * 8) == cudaSuccess ? 1 : 0;
+    cudaGetLastError();
+  }
+  if (!ok) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, jacobi_sq2_kernel<NT, K>, in, U, s, Vt, tol, jacobi_dbg());
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  QTT_CHECK_LAUNCH();
+  return true;
+}
+
 // n <= 16 K: 8 lanes per pair, ceil(n/2) <= 8 K pairs -> NT = 64 K threads
 template <int NT, int K>
 static void jacobi_sq_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt, double tol, size_t bytes) {
@@ -762,6 +1025,21 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   if (sq && m == n && n <= 112) {
     const int K = cdiv(n, 16);
     const size_t bytes = ((size_t)32 * K * n + n) * sizeof(double);
+    // two CTAs (W | V) from n = 81 on (200 x 100: 2.48 -> 2.14 ms); below, a round is latency-
+    // rather than shared-memory-bound and the split does not pay (136 x 68: 1.09 -> 1.13 ms).
+    // QTT_JAC_SQ2 = smallest K = ceil(n / 16) that takes the cluster kernel (0: never).
+    static const int sq2 = std::getenv("QTT_JAC_SQ2") ? std::atoi(std::getenv("QTT_JAC_SQ2")) : 6;
+    if (sq2 > 0 && K >= std::max(3, sq2)) {
+      bool done = false;
+      switch (K) {
+        case 3: done = jacobi_sq2_launch<192, 3>(c, in, U, s, Vt, tol); break;
+        case 4: done = jacobi_sq2_launch<256, 4>(c, in, U, s, Vt, tol); break;
+        case 5: done = jacobi_sq2_launch<320, 5>(c, in, U, s, Vt, tol); break;
+        case 6: done = jacobi_sq2_launch<384, 6>(c, in, U, s, Vt, tol); break;
+        default: done = jacobi_sq2_launch<448, 7>(c, in, U, s, Vt, tol); break;
+      }
+      if (done) return;
+    }
     switch (K) {
       case 1: jacobi_sq_launch<64, 1>(c, in, U, s, Vt, tol, bytes); break;
       case 2: jacobi_sq_launch<128, 2>(c, in, U, s, Vt, tol, bytes); break;

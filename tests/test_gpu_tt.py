@@ -1,6 +1,7 @@
 """GPU parity of the dense factorizations (K6/K7), TT algebra (K9/K10, rounding)
 and the local solvers (K4/K5) against the reference fixtures and the oracle."""
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -119,6 +120,34 @@ def test_svd_matches_numpy(tt, shape):
     else:
         assert np.linalg.norm(vt @ vt.T - np.eye(k)) <= 1e-12 * k
         assert np.linalg.norm(u[:, :big].T @ u[:, :big] - np.eye(big)) <= 1e-12 * k
+
+
+def test_svd_two_cta_jacobi_same_bits_as_one_cta():
+    """The 2-CTA Jacobi (W and its angles in one CTA, V one DSMEM hop behind in the other,
+    linalg.cu jacobi_sq2_kernel) performs the floating-point operations of the one-CTA kernel in
+    the same order: U, s, Vt equal bit for bit.  (QTT_JAC_SQ2 is read once per process: one
+    child process per setting; 3 = every width the cluster kernel supports, 0 = never.)"""
+    import subprocess
+    import sys
+    code = (
+        "import sys, hashlib, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2501_12151_b200 import tt\n"
+        "h = hashlib.sha256()\n"
+        "for m, n in [(200, 100), (100, 100), (224, 112), (96, 81), (130, 65), (90, 40), (70, 33)]:\n"
+        "    rng = np.random.default_rng(m * 7 + n)\n"
+        "    a = rng.standard_normal((m, n)) * np.logspace(0, -8, n)[None, :]\n"
+        "    for x in tt._svd(a):\n"
+        "        h.update(np.ascontiguousarray(x).tobytes())\n"
+        "print(h.hexdigest())\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for setting in ("0", "3"):
+        env = dict(os.environ, QTT_JAC_SQ2=setting)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[setting] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["3"], out
 
 
 def test_truncated_factor_ranks_vs_reference(tt):
