@@ -19,6 +19,17 @@
 #pragma once
 #include "tma_tile.cuh"
 
+// tools/tile_bench.cu builds the engine with -DQTT_FB_NOLOAD (no TMA copies: stale operands) and
+// -DQTT_FB_NOSYNC (no mbarrier traffic at all) to separate the cost of the data supply and of the
+// ring handshake from the consumer instruction stream itself.
+#ifdef QTT_FB_NOSYNC
+#define QTT_FB_WAIT(bar, parity) ((void)0)
+#define QTT_FB_ARRIVE(bar) ((void)0)
+#else
+#define QTT_FB_WAIT(bar, parity) tma::mbar_wait(bar, parity)
+#define QTT_FB_ARRIVE(bar) tma::mbar_arrive(bar)
+#endif
+
 namespace qtt {
 namespace tmafb {
 
@@ -85,10 +96,10 @@ struct Boxes {
 // Fill stage s (fill parity ph) with k-tile kt of region g: wait until every consumer warp
 // released the stage's previous fill (a fresh barrier passes the parity-1 wait at once).
 __device__ __forceinline__ void issue(Ring& r, int s, unsigned ph, const Boxes& bx, const Region& g, int kt) {
-  tma::mbar_wait(&r.empty[s], ph ^ 1u);
+  QTT_FB_WAIT(&r.empty[s], ph ^ 1u);
   unsigned char* st = r.base + (size_t)s * r.stride;
 #ifdef QTT_FB_NOLOAD  // tools/tile_bench.cu: the loop without the TMA copies (stale operands)
-  tma::mbar_arrive(&r.full[s]);
+  QTT_FB_ARRIVE(&r.full[s]);
   (void)st;
 #else
   tma::mbar_expect_tx(&r.full[s], (bx.box_a + bx.box_b) * 128);
@@ -255,7 +266,7 @@ __device__ __forceinline__ void stream(Ring& r, const Boxes& bx, int n, Get get,
     for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
     Operands<NF, DEDUPE> o;
     // region prologue: the operands of its first k-step
-    tma::mbar_wait(&r.full[cs], cph);
+    QTT_FB_WAIT(&r.full[cs], cph);
     if (tl && ci == 0) r.dbg[4 * r.dbg_slot] += fb_clock() - t_start;
     load_step<NF, DEDUPE>(r, cs, 0, bx, fr, o);
     for (int ck = Cur.kb; ck + 1 < Cur.ke; ++ck) {
@@ -269,11 +280,12 @@ __device__ __forceinline__ void stream(Ring& r, const Boxes& bx, int n, Get get,
         ns = 0;
         cph ^= 1u;
       }
-      // the last k-step loads from the next k-tile: pass its full barrier now
-      tma::mbar_wait(&r.full[ns], cph);
+      // the last k-step loads from the next k-tile: pass its full barrier now (probing it three
+      // k-steps earlier and waiting only on a failed probe measured the same)
+      QTT_FB_WAIT(&r.full[ns], cph);
       step<NF, DEDUPE, true>(r, cs, 3, ns, 0, bx, fr, o, acc);
       __syncwarp();
-      if (lane == 0) tma::mbar_arrive(&r.empty[cs]);
+      if (lane == 0) QTT_FB_ARRIVE(&r.empty[cs]);
       cs = ns;
     }
     {  // the region's last k-tile
@@ -284,7 +296,7 @@ __device__ __forceinline__ void stream(Ring& r, const Boxes& bx, int n, Get get,
       step<NF, DEDUPE, true>(r, cs, 2, cs, 3, bx, fr, o, acc);
       step<NF, DEDUPE, false>(r, cs, 3, cs, 0, bx, fr, o, acc);
       __syncwarp();
-      if (lane == 0) tma::mbar_arrive(&r.empty[cs]);
+      if (lane == 0) QTT_FB_ARRIVE(&r.empty[cs]);
       if (++cs == nst) {
         cs = 0;
         cph ^= 1u;
