@@ -11,6 +11,25 @@
 namespace cg = cooperative_groups;
 
 __device__ unsigned g_count, g_flag;
+__device__ unsigned g_flags[1024 * 8];  // mode 3/4: one epoch word per CTA (packed / one per 32-byte sector)
+
+// mode 3/4: no atomics.  Thread 0 publishes the CTA's epoch with st.release.gpu; thread i polls
+// CTA i's word with ld.acquire.gpu until it reaches the epoch; block barrier.  The 148 arrivals do
+// not serialise on one L2 address as the counter's atomics do.
+template <int STRIDE>
+__device__ __forceinline__ void bar3(unsigned nblocks, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0)
+    asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&g_flags[blockIdx.x * STRIDE]), "r"(epoch) : "memory");
+  for (unsigned i = threadIdx.x; i < nblocks; i += blockDim.x) {
+    unsigned f;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(f) : "l"(&g_flags[i * STRIDE]) : "memory");
+    } while ((int)(f - epoch) < 0);
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ void bar1(unsigned nblocks, unsigned& sense) {
   __syncthreads();
@@ -49,6 +68,8 @@ __global__ void kern(int iters, int mode, double* sink) {
     acc = acc * 1.0000001 + 1.0;
     if (mode == 0) cg::this_grid().sync();
     else if (mode == 1) bar1(gridDim.x, sense);
+    else if (mode == 3) bar3<1>(gridDim.x, sense);
+    else if (mode == 4) bar3<8>(gridDim.x, sense);
     else bar2(gridDim.x / 2, sense);
   }
   if (acc == -1.0) sink[0] = acc;
@@ -59,7 +80,13 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* sink;
   cudaMalloc(&sink, 8);
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode : {0, 1, 3, 4}) {
+    cudaMemset(nullptr, 0, 0);
+    {
+      void* p = nullptr;
+      cudaGetSymbolAddress(&p, g_flags);
+      cudaMemset(p, 0, sizeof(unsigned) * 1024 * 8);
+    }
     for (int nt : {128, 384}) {
       int iters = 20000;
       void* args[] = {&iters, &mode, &sink};
