@@ -148,21 +148,24 @@ __device__ __noinline__ tmafb::Ring phase1_t(const CGTmaArgs& a, const CUtensorM
   const int RB = a.p1_rb, CB = a.p1_cb;
   const int nrb = (r1 - r0 + RB - 1) / RB, ncb = (FC + CB - 1) / CB;
   const tmafb::Boxes bx{&a.map_bop, mv, a.box1_a, a.box1_b};
-  // p1_frun: one region per CTA, its exact 1/G share of ALL fragments (row-major run)
+  // p1_frun > 0: every CTA owns its exact 1/G share of ALL fragments (a row-major run), streamed
+  // as p1_frun regions (one while the share fits the warps' accumulators)
   const long long Fall = (long long)FR * FC;
   const int fb_all = (int)(Fall * c / G), fe_all = (int)(Fall * (c + 1) / G);
   auto get = [&](int i) {
     tmafb::Region g;
     g.kb = 0;
     g.ke = KT;
-    if (a.p1_frun) {
-      const int fr0 = fb_all / FC, fr1 = (fe_all - 1) / FC + 1;
+    if (a.p1_frun) {  // chunk i of this CTA's fragment run (p1_frun chunks of equal length)
+      const int chunk = (fe_all - fb_all + a.p1_frun - 1) / a.p1_frun;
+      const int fb = fb_all + i * chunk, fe = min(fe_all, fb + chunk);
+      const int fr0 = fb / FC, fr1 = (fe - 1) / FC + 1;
       g.m0 = fr0 * 8;
       g.mrows = (fr1 - fr0) * 8;
       g.n0 = 0;
       g.ncols = FC * 8;
-      g.fb = fb_all - fr0 * FC;
-      g.fe = fe_all - fr0 * FC;
+      g.fb = fb - fr0 * FC;
+      g.fe = fe - fr0 * FC;
       return g;
     }
     const int rb = i / ncb, cb = i - (i / ncb) * ncb;
@@ -183,7 +186,11 @@ __device__ __noinline__ tmafb::Ring phase1_t(const CGTmaArgs& a, const CUtensorM
       return t2 + xm * K3p + (long long)bb * rk;
     });
   };
-  const int nreg = a.p1_frun ? (fe_all > fb_all ? 1 : 0) : (r1 > r0 ? nrb * ncb : 0);
+  int nreg = r1 > r0 ? nrb * ncb : 0;
+  if (a.p1_frun) {  // non-empty chunks
+    const int len = fe_all - fb_all, chunk = (len + a.p1_frun - 1) / a.p1_frun;
+    nreg = len > 0 ? (len + chunk - 1) / chunk : 0;
+  }
   tmafb::stream<NF, DEDUPE>(ring, bx, nreg, get, epi);
   return ring;
 }
@@ -501,12 +508,26 @@ CGTmaPlan cg_tma_plan(int lb, int m, int R1, int lk, int n, int rb, int rk, int 
       rmax = std::max(rmax, (fe - 1) / FC1 - fb / FC1 + 1);
     }
     static const int frun_env = std::getenv("QTT_TMA_FRUN") ? std::atoi(std::getenv("QTT_TMA_FRUN")) : 1;
-    if (frun_env && FC1 <= 32 && fmax > 0 && fmax <= FMAX && rmax <= 32 && (rmax + FC1) * 8 * 128 <= 48 * 1024) {
-      p.p1_frun = 1;
+    // shares beyond 10 fragments per warp (the largest variant that neither spills nor leaves a
+    // tail region half empty: C5, rank 196, 430 fragments per CTA) are cut into equal chunks
+    const int chunks = fmax > 0 ? cdiv(fmax, 10 * tmafb::NWARP) : 1;
+    const int cmax = fmax > 0 ? cdiv(fmax, chunks) : 0;
+    int rmax_c = 1;
+    for (int c = 0; c < grid && chunks > 1; ++c) {
+      const int fb = (int)(Fall * c / grid), fe = (int)(Fall * (c + 1) / grid);
+      const int chunk = cdiv(fe - fb, chunks);
+      for (int i = 0; i < chunks && chunk > 0; ++i) {
+        const int b = fb + i * chunk, e = std::min(fe, b + chunk);
+        if (e > b) rmax_c = std::max(rmax_c, (e - 1) / FC1 - b / FC1 + 1);
+      }
+    }
+    if (chunks == 1) rmax_c = rmax;
+    if (frun_env && FC1 <= 32 && fmax > 0 && chunks <= 16 && rmax_c <= 32 && (rmax_c + FC1) * 8 * 128 <= 48 * 1024) {
+      p.p1_frun = chunks;
       p.p1_cb = FC1;
-      p.box1_a = rmax * 8;
+      p.box1_a = rmax_c * 8;
       p.box1_b = FC1 * 8;
-      p.p1_nf = tmafb::nf_for(fmax);
+      p.p1_nf = tmafb::nf_for(cmax);
       p.p1_dedupe = tmafb::dedupe_ok(p.p1_nf, FC1) ? 1 : 0;
     }
   }
