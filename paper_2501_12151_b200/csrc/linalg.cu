@@ -751,7 +751,7 @@ static void jacobi_launch(Ctx& c, CMatView in, MatView U, double* s, MatView Vt,
 // Every floating-point operation and its order are those of jacobi_sq_kernel: same bits.
 namespace jq2 {
 constexpr int DEPTH = 8;     // ring slots
-constexpr int MAXG = 64;     // rotation groups per round (<= 56)
+constexpr int MAXG = 80;     // rotation groups per round (<= 8 K = 80)
 struct Mail {                // lives in CTA 1's shared memory (CTA 0 writes it remotely)
   double cs[DEPTH][MAXG];
   double sn[DEPTH][MAXG];
@@ -972,8 +972,9 @@ static bool jacobi_sq2_launch(Ctx& c, CMatView in, MatView U, double* s, MatView
   int& ok = ok_dev();
   const size_t bytes = ((size_t)16 * K * in.cols + in.cols) * sizeof(double);
   if (ok < 0) {
+    // the widest matrix of this K (n = 16 K) next to ~11 KB of static shared memory (the mail box)
     ok = cudaFuncSetAttribute(jacobi_sq2_kernel<NT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kSmemDoubles * 8) == cudaSuccess ? 1 : 0;
+                              (int)(((size_t)16 * K * 16 * K + 16 * K) * sizeof(double))) == cudaSuccess ? 1 : 0;
     cudaGetLastError();
   }
   if (!ok) return false;
@@ -1022,6 +1023,10 @@ static void jacobi(Ctx& c, CMatView in, MatView U, double* s, MatView Vt) {
   }
   const double tol = std::sqrt((double)m) * 2.220446049250313e-16;
   static const int sq = std::getenv("QTT_JAC_SQ") ? std::atoi(std::getenv("QTT_JAC_SQ")) : 1;
+  // (The 2-CTA kernel also fits widths 113..144 -- W alone and V alone fit a CTA's shared memory --
+  // and is faster there than the block Jacobi, tools/svd_mid2.py: n = 120 2.22 vs 2.83 ms, 140
+  // 2.85 vs 3.45; it loses from 150 on.  Not routed: 0.09 s of C5's 1.8 s SVD phase, and another
+  // SVD algorithm at those widths moves C5's trajectory.)
   if (sq && m == n && n <= 112) {
     const int K = cdiv(n, 16);
     const size_t bytes = ((size_t)32 * K * n + n) * sizeof(double);
